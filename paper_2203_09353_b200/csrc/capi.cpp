@@ -1,0 +1,511 @@
+// capi.cpp — host side of the C ABI (include/taskgemm_b200.h).
+//
+// Replaces, for ExecutionMode::kDevice, the reference's annealing driver
+// (bench::run_experiment, bench.cpp:341-417) and GEMM batcher (VirtualDevice::batched_gemm,
+// exec.cpp:144-221): configuration validation with the reference's messages, the
+// p -> device binding (bench.cpp:171), one host thread per GPU, one persistent kernel per
+// GPU, trace copy-back and the procedure-order average (spinmc.cpp:253-269). There is no
+// CPU fallback: without a CUDA device every entry point fails with TG_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/taskgemm_b200.h"
+#include "tg_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+tg_status fail(tg_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+tg_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(TG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define TG_CUDA(call)                                         \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);       \
+  } while (0)
+
+struct DeviceState {
+  int ordinal = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // grow-only device buffers reused across calls
+  void* trace = nullptr;
+  size_t trace_bytes = 0;
+  void* workspace = nullptr;
+  size_t workspace_bytes = 0;
+};
+
+}  // namespace
+
+struct tg_ctx {
+  std::vector<DeviceState> devs;
+  std::mutex mu;
+  bool shutdown = false;
+};
+
+namespace {
+
+uint64_t rows_for(const tg_anneal_config* c) {
+  const uint64_t sc = c->shard_count ? c->shard_count : 1;
+  if (c->shard_index >= c->procedures) return 0;
+  return (c->procedures - c->shard_index + sc - 1) / sc;
+}
+
+// bench::validate (bench.cpp:321-329) + dims_for_spins (spinmc.cpp:15-26) + device tiers.
+tg_status validate(const tg_anneal_config* c) {
+  if (!c) return fail(TG_EINVAL, "config must not be NULL");
+  if (c->spins < 2 || c->spins > 30)
+    return fail(TG_ECONFIG, "spins out of range [2,30]: " + std::to_string(c->spins));
+  if (c->procedures < 1) return fail(TG_ECONFIG, "procedures must be >= 1");
+  if (c->devices < 1) return fail(TG_ECONFIG, "devices must be >= 1");
+  if (!(c->t0 > 0.0) || !(c->t_min > 0.0) || c->t_min > c->t0)
+    return fail(TG_ECONFIG, "anneal schedule requires 0 < t_min <= t0");
+  const uint32_t sc = c->shard_count ? c->shard_count : 1;
+  if (c->shard_index >= sc) return fail(TG_ECONFIG, "shard_index must be < shard_count");
+  if (c->spins > 24)
+    return fail(TG_EINVAL, "device tiers cover spins <= 24 (state of 2^" + std::to_string(c->spins) +
+                               " amplitudes per replica)");
+  if (c->entropy_kind != TG_RENYI2)
+    return fail(TG_EINVAL,
+                "device path computes renyi-2 entropy only (von-neumann is the next row, DESIGN.md)");
+  if (c->objective != TG_MAXIMIZE && c->objective != TG_MINIMIZE)
+    return fail(TG_ECONFIG, "objective must be max or min");
+  if (c->initial_state != TG_PRODUCT && c->initial_state != TG_RANDOM)
+    return fail(TG_ECONFIG, "initial_state must be product or random");
+  if (c->steps > (uint64_t{1} << 40)) return fail(TG_ECONFIG, "steps too large");
+  return TG_OK;
+}
+
+tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t p_first,
+                             uint64_t p_stride) {
+  tg::AnnealParams p{};
+  p.spins = c->spins;
+  p.objective = c->objective;
+  p.initial_state = c->initial_state;
+  p.inject_fault = c->inject_fault;
+  p.steps = c->steps;
+  p.seed = c->seed;
+  p.renorm = c->renormalize_interval;
+  p.t0 = c->t0;
+  p.t_min = c->t_min;
+  p.rows = rows;
+  p.p_first = p_first;
+  p.p_stride = p_stride;
+  return p;
+}
+
+cudaError_t launch(const tg::AnnealParams& p, cudaStream_t s) {
+  return p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::launch_anneal_smem(p, s, nullptr)
+                                                            : tg::launch_anneal_hbm(p, s, nullptr);
+}
+
+template <class T>
+T* carve(char*& cursor, size_t count) {
+  cursor = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(cursor) + 255) & ~uintptr_t{255});
+  T* p = reinterpret_cast<T*>(cursor);
+  cursor += count * sizeof(T);
+  return p;
+}
+
+size_t trace_bytes(uint64_t rows, uint64_t steps, bool sites, bool wall) {
+  const size_t rs = rows * steps;
+  return rows * (8 + 8 + 4 + 8) + rs * (8 + 1) + (sites ? rs : 0) + (wall ? rs * 8 : 0) + 8 * 256;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tg_last_error(void) { return g_err.c_str(); }
+const char* tg_version(void) { return "taskgemm-b200 0.1 (sm_100a, DMMA.8x8x4 persistent anneal)"; }
+
+uint64_t tg_anneal_rows(const tg_anneal_config* cfg) { return cfg ? rows_for(cfg) : 0; }
+
+uint64_t tg_step_flops(uint32_t spins) {
+  if (spins < 2 || spins > 30) return 0;
+  const uint64_t da = uint64_t{1} << (spins / 2), db = uint64_t{1} << (spins - spins / 2);
+  return 8ull * da * da * db;  // gemm_flops(d_a, d_a, d_b), linalg.cpp:140-144
+}
+
+tg_status tg_validate(const tg_anneal_config* cfg) { return validate(cfg); }
+
+tg_status tg_create(const int* gpus, int n, tg_ctx** out) {
+  if (!out) return fail(TG_EINVAL, "out must not be NULL");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(TG_ECUDA, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                              "); the device path has no CPU fallback");
+  if (n < 1) return fail(TG_ECONFIG, "devices must be >= 1");
+  auto ctx = std::make_unique<tg_ctx>();
+  for (int i = 0; i < n; ++i) {
+    DeviceState d;
+    d.ordinal = gpus ? gpus[i] : i;
+    if (d.ordinal < 0 || d.ordinal >= count)
+      return fail(TG_ECONFIG, "GPU ordinal " + std::to_string(d.ordinal) + " out of range (" +
+                                  std::to_string(count) + " visible)");
+    TG_CUDA(cudaSetDevice(d.ordinal));
+    TG_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    TG_CUDA(cudaEventCreate(&d.ev0));
+    TG_CUDA(cudaEventCreate(&d.ev1));
+    ctx->devs.push_back(d);
+  }
+  *out = ctx.release();
+  return TG_OK;
+}
+
+tg_status tg_shutdown(tg_ctx* ctx) {
+  if (!ctx) return fail(TG_EINVAL, "ctx must not be NULL");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  ctx->shutdown = true;
+  return TG_OK;
+}
+
+tg_status tg_destroy(tg_ctx* ctx) {
+  if (!ctx) return TG_OK;
+  for (auto& d : ctx->devs) {
+    cudaSetDevice(d.ordinal);
+    cudaStreamSynchronize(d.stream);
+    if (d.trace) cudaFree(d.trace);
+    if (d.workspace) cudaFree(d.workspace);
+    cudaEventDestroy(d.ev0);
+    cudaEventDestroy(d.ev1);
+    cudaStreamDestroy(d.stream);
+  }
+  delete ctx;
+  return TG_OK;
+}
+
+size_t tg_anneal_workspace_bytes(const tg_anneal_config* cfg) {
+  if (!cfg || cfg->spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) || cfg->spins > 24) return 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return tg::anneal_hbm_workspace_bytes(cfg->spins, rows_for(cfg), dev);
+}
+
+tg_status tg_anneal_launch(const tg_anneal_config* cfg, const tg_anneal_device_buffers* b,
+                           void* stream) {
+  if (tg_status s = validate(cfg)) return s;
+  if (!b || !b->initial_entropy || !b->entropies || !b->accepted || !b->final_entropy ||
+      !b->status || !b->status_step)
+    return fail(TG_EINVAL, "device buffers initial_entropy/entropies/accepted/final_entropy/status "
+                           "must not be NULL");
+  const uint64_t rows = rows_for(cfg);
+  tg::AnnealParams p = make_params(cfg, rows, cfg->shard_index, cfg->shard_count ? cfg->shard_count : 1);
+  p.initial_entropy = b->initial_entropy;
+  p.entropies = b->entropies;
+  p.accepted = b->accepted;
+  p.sites = b->sites;
+  p.wall_ns = b->wall_ns;
+  p.final_entropy = b->final_entropy;
+  p.status = b->status;
+  p.status_step = b->status_step;
+  p.workspace = static_cast<double*>(b->workspace);
+  if (cfg->spins > static_cast<uint32_t>(tg::kSmemMaxSpins) && !p.workspace)
+    return fail(TG_EINVAL, "workspace required for spins > 12 (tg_anneal_workspace_bytes)");
+  cudaError_t e = launch(p, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "anneal launch");
+  return TG_OK;
+}
+
+tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_result* res) {
+  if (!ctx) return fail(TG_EINVAL, "ctx must not be NULL");
+  if (tg_status s = validate(cfg)) return s;
+  if (!res || !res->initial_entropy || !res->entropies || !res->accepted)
+    return fail(TG_EINVAL, "result arrays initial_entropy/entropies/accepted must not be NULL");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (ctx->shutdown) return fail(TG_ESHUTDOWN, "VirtualDevice: submit after shutdown");
+  if (cfg->devices > ctx->devs.size())
+    return fail(TG_ECONFIG, "devices (" + std::to_string(cfg->devices) + ") exceeds the context's " +
+                                std::to_string(ctx->devs.size()) + " GPUs");
+  const auto t_begin = std::chrono::steady_clock::now();
+  const uint64_t rows = rows_for(cfg);
+  const uint64_t D = cfg->devices;
+  const uint64_t sc = cfg->shard_count ? cfg->shard_count : 1;
+  const uint64_t steps = cfg->steps;
+  const bool want_sites = res->sites != nullptr, want_wall = res->wall_ns != nullptr;
+
+  std::vector<tg_status> st(D, TG_OK);
+  std::vector<std::string> msg(D);
+  std::vector<float> ms(D, 0.f);
+  std::vector<std::vector<int32_t>> status(D);
+  std::vector<std::vector<int64_t>> status_step(D);
+  std::vector<std::vector<double>> finals(D);
+
+  auto worker = [&](uint64_t g) {
+    DeviceState& d = ctx->devs[g];
+    auto err = [&](tg_status s, const std::string& m) {
+      st[g] = s;
+      msg[g] = m;
+    };
+    auto cu = [&](cudaError_t e, const char* w) {
+      if (e != cudaSuccess) err(TG_ECUDA, std::string(w) + ": " + cudaGetErrorString(e));
+      return e == cudaSuccess;
+    };
+    if (!cu(cudaSetDevice(d.ordinal), "cudaSetDevice")) return;
+    const uint64_t lrows = rows > g ? (rows - g + D - 1) / D : 0;
+    if (lrows == 0) return;
+    // device buffers (grow-only)
+    const size_t need = trace_bytes(lrows, steps, want_sites, want_wall);
+    if (need > d.trace_bytes) {
+      if (d.trace) cudaFree(d.trace);
+      d.trace = nullptr;
+      d.trace_bytes = 0;
+      if (!cu(cudaMalloc(&d.trace, need), "cudaMalloc(traces)")) return;
+      d.trace_bytes = need;
+    }
+    char* cur = static_cast<char*>(d.trace);
+    tg::AnnealParams p = make_params(cfg, lrows, cfg->shard_index + g * sc, D * sc);
+    p.initial_entropy = carve<double>(cur, lrows);
+    p.final_entropy = carve<double>(cur, lrows);
+    p.status = carve<int32_t>(cur, lrows);
+    p.status_step = carve<int64_t>(cur, lrows);
+    p.entropies = carve<double>(cur, lrows * steps);
+    p.accepted = carve<uint8_t>(cur, lrows * steps);
+    p.sites = want_sites ? carve<uint8_t>(cur, lrows * steps) : nullptr;
+    p.wall_ns = want_wall ? carve<int64_t>(cur, lrows * steps) : nullptr;
+    if (cfg->spins > static_cast<uint32_t>(tg::kSmemMaxSpins)) {
+      const size_t ws = tg::anneal_hbm_workspace_bytes(cfg->spins, lrows, d.ordinal);
+      if (ws > d.workspace_bytes) {
+        if (d.workspace) cudaFree(d.workspace);
+        d.workspace = nullptr;
+        d.workspace_bytes = 0;
+        if (!cu(cudaMalloc(&d.workspace, ws), "cudaMalloc(workspace)")) return;
+        d.workspace_bytes = ws;
+      }
+      p.workspace = static_cast<double*>(d.workspace);
+    }
+    if (!cu(cudaEventRecord(d.ev0, d.stream), "cudaEventRecord")) return;
+    if (!cu(launch(p, d.stream), "anneal launch")) return;
+    if (!cu(cudaEventRecord(d.ev1, d.stream), "cudaEventRecord")) return;
+    // copy back: rows of this GPU are host rows g + D*q
+    std::vector<double> init(lrows), fin(lrows), ent(lrows * steps);
+    std::vector<uint8_t> acc(lrows * steps), sit(want_sites ? lrows * steps : 0);
+    std::vector<int64_t> wall(want_wall ? lrows * steps : 0);
+    status[g].resize(lrows);
+    status_step[g].resize(lrows);
+    bool ok = cu(cudaMemcpyAsync(init.data(), p.initial_entropy, 8 * lrows, cudaMemcpyDeviceToHost, d.stream), "D2H") &&
+              cu(cudaMemcpyAsync(fin.data(), p.final_entropy, 8 * lrows, cudaMemcpyDeviceToHost, d.stream), "D2H") &&
+              cu(cudaMemcpyAsync(status[g].data(), p.status, 4 * lrows, cudaMemcpyDeviceToHost, d.stream), "D2H") &&
+              cu(cudaMemcpyAsync(status_step[g].data(), p.status_step, 8 * lrows, cudaMemcpyDeviceToHost, d.stream), "D2H");
+    if (ok && steps > 0) {
+      // D == 1 and host rows contiguous: copy straight into the caller's arrays
+      double* ent_dst = D == 1 ? res->entropies : ent.data();
+      uint8_t* acc_dst = D == 1 ? res->accepted : acc.data();
+      ok = cu(cudaMemcpyAsync(ent_dst, p.entropies, 8 * lrows * steps, cudaMemcpyDeviceToHost, d.stream), "D2H") &&
+           cu(cudaMemcpyAsync(acc_dst, p.accepted, lrows * steps, cudaMemcpyDeviceToHost, d.stream), "D2H");
+      if (ok && want_sites)
+        ok = cu(cudaMemcpyAsync(D == 1 ? res->sites : sit.data(), p.sites, lrows * steps, cudaMemcpyDeviceToHost, d.stream), "D2H");
+      if (ok && want_wall)
+        ok = cu(cudaMemcpyAsync(D == 1 ? res->wall_ns : wall.data(), p.wall_ns, 8 * lrows * steps, cudaMemcpyDeviceToHost, d.stream), "D2H");
+    }
+    if (!ok) return;
+    if (!cu(cudaStreamSynchronize(d.stream), "anneal kernel")) return;
+    cudaEventElapsedTime(&ms[g], d.ev0, d.ev1);
+    for (uint64_t q = 0; q < lrows; ++q) {
+      const uint64_t hr = g + D * q;
+      res->initial_entropy[hr] = init[q];
+      if (res->final_entropy) res->final_entropy[hr] = fin[q];
+      if (D > 1 && steps > 0) {
+        std::memcpy(res->entropies + hr * steps, ent.data() + q * steps, 8 * steps);
+        std::memcpy(res->accepted + hr * steps, acc.data() + q * steps, steps);
+        if (want_sites) std::memcpy(res->sites + hr * steps, sit.data() + q * steps, steps);
+        if (want_wall) std::memcpy(res->wall_ns + hr * steps, wall.data() + q * steps, 8 * steps);
+      }
+    }
+    finals[g] = std::move(fin);
+  };
+
+  if (D == 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> th;
+    for (uint64_t g = 0; g < D; ++g) th.emplace_back(worker, g);
+    for (auto& t : th) t.join();
+  }
+  for (uint64_t g = 0; g < D; ++g)
+    if (st[g] != TG_OK) return fail(st[g], msg[g]);
+  // first failing replica in procedure order -> KernelError (exec.hpp:76-86)
+  for (uint64_t hr = 0; hr < rows; ++hr) {
+    const uint64_t g = hr % D, q = hr / D;
+    if (status[g][q] != tg::kRowOk) {
+      const uint64_t p = cfg->shard_index + hr * sc;
+      const int64_t s = status_step[g][q];
+      return fail(TG_EKERNEL, "kernel failed for procedure " + std::to_string(p) +
+                                  ": entanglement_entropy: state not normalized (" +
+                                  (s < 0 ? std::string("initial state") : "step " + std::to_string(s)) + ")");
+    }
+  }
+  double sum = 0.0;  // procedure order, spinmc.cpp:259-268 / bench.cpp:401-407
+  for (uint64_t hr = 0; hr < rows; ++hr)
+    sum += steps > 0 ? finals[hr % D][hr / D] : res->initial_entropy[hr];
+  res->average_entropy = rows ? sum / static_cast<double>(rows) : 0.0;
+  res->total_flops = (rows * steps + rows) * tg_step_flops(cfg->spins);
+  res->kernel_ms = *std::max_element(ms.begin(), ms.end());
+  res->total_wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                           std::chrono::steady_clock::now() - t_begin)
+                           .count();
+  return TG_OK;
+}
+
+tg_status tg_zgemm_strided_launch(int batch, int m, int n, int k, const double alpha[2],
+                                  const double* A, int64_t sA, const double* B, int64_t sB,
+                                  const double beta[2], const double* C, int64_t sC, double* out,
+                                  int64_t sO, int inject_fault, void* stream) {
+  if (batch < 1) return fail(TG_EINVAL, "batched_gemm: batch must be non-empty");
+  if (m < 1 || n < 1 || k < 1) return fail(TG_EINVAL, "gemm: dims must be >= 1");
+  if (!alpha || !beta || !A || !B || !out) return fail(TG_EINVAL, "gemm: NULL operand");
+  cudaError_t e = tg::launch_zgemm_strided(batch, m, n, k, alpha[0], alpha[1], A, sA, B, sB, beta[0],
+                                           beta[1], C, sC, out, sO, inject_fault,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "zgemm launch");
+  return TG_OK;
+}
+
+tg_status tg_zgemm_batched(tg_ctx* ctx, int device, int batch, int m, int n, int k,
+                           const double alpha[2], const double* const* A, const double* const* B,
+                           const double beta[2], const double* const* C, double* const* out,
+                           const uint64_t* procedures, tg_kernel_record* records) {
+  if (!ctx) return fail(TG_EINVAL, "ctx must not be NULL");
+  if (batch < 1) return fail(TG_EINVAL, "batched_gemm: batch must be non-empty");
+  if (m < 1 || n < 1 || k < 1) return fail(TG_EINVAL, "gemm: dims must be >= 1");
+  if (!alpha || !beta || !A || !B || !out) return fail(TG_EINVAL, "gemm: NULL operand");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (ctx->shutdown) return fail(TG_ESHUTDOWN, "VirtualDevice: submit after shutdown");
+  if (device < 0 || static_cast<size_t>(device) >= ctx->devs.size())
+    return fail(TG_EINVAL, "device index out of range");
+  DeviceState& d = ctx->devs[device];
+  TG_CUDA(cudaSetDevice(d.ordinal));
+  const size_t ea = 2ull * m * k, eb = 2ull * k * n, ec = 2ull * m * n;
+  const bool has_c = C != nullptr;
+  const size_t bytes = 8 * static_cast<size_t>(batch) * (ea + eb + (has_c ? ec : 0) + ec);
+  const auto t0 = std::chrono::steady_clock::now();
+  double* buf = nullptr;
+  TG_CUDA(cudaMallocAsync(&buf, bytes, d.stream));
+  double *dA = buf, *dB = dA + batch * ea, *dC = has_c ? dB + batch * eb : nullptr;
+  double* dO = (has_c ? dC + batch * ec : dB + batch * eb);
+  for (int i = 0; i < batch; ++i) {
+    TG_CUDA(cudaMemcpyAsync(dA + i * ea, A[i], 8 * ea, cudaMemcpyHostToDevice, d.stream));
+    TG_CUDA(cudaMemcpyAsync(dB + i * eb, B[i], 8 * eb, cudaMemcpyHostToDevice, d.stream));
+    if (has_c) TG_CUDA(cudaMemcpyAsync(dC + i * ec, C[i], 8 * ec, cudaMemcpyHostToDevice, d.stream));
+  }
+  TG_CUDA(cudaEventRecord(d.ev0, d.stream));
+  cudaError_t e = tg::launch_zgemm_strided(batch, m, n, k, alpha[0], alpha[1], dA, ea / 2, dB, eb / 2,
+                                           beta[0], beta[1], dC, ec / 2, dO, ec / 2, 0, d.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "zgemm launch");
+  TG_CUDA(cudaEventRecord(d.ev1, d.stream));
+  for (int i = 0; i < batch; ++i)
+    TG_CUDA(cudaMemcpyAsync(out[i], dO + i * ec, 8 * ec, cudaMemcpyDeviceToHost, d.stream));
+  TG_CUDA(cudaFreeAsync(buf, d.stream));
+  TG_CUDA(cudaStreamSynchronize(d.stream));
+  float kms = 0.f;
+  cudaEventElapsedTime(&kms, d.ev0, d.ev1);
+  const auto t1 = std::chrono::steady_clock::now();
+  if (records) {
+    const int64_t exec_ns = std::max<int64_t>(1, static_cast<int64_t>(kms * 1e6 / batch));
+    const int64_t wait_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count() -
+                            static_cast<int64_t>(kms * 1e6);
+    for (int i = 0; i < batch; ++i) {
+      records[i].device_id = static_cast<uint64_t>(device);
+      records[i].procedure = procedures ? procedures[i] : static_cast<uint64_t>(i);
+      records[i].m = m;
+      records[i].n = n;
+      records[i].k = k;
+      records[i].queue_wait_ns = std::max<int64_t>(0, wait_ns);
+      records[i].exec_time_ns = exec_ns;
+      records[i].flops = 8ull * m * n * k;
+    }
+  }
+  return TG_OK;
+}
+
+tg_status tg_fp64_dmma_peak(int device, double* tflops, double* clock_ghz) {
+  if (!tflops) return fail(TG_EINVAL, "tflops must not be NULL");
+  TG_CUDA(cudaSetDevice(device));
+  TG_CUDA(tg::fp64_dmma_peak(tflops, clock_ghz));
+  return TG_OK;
+}
+
+// ------------------------------------------------------------------------- probes
+tg_status tg_probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* out) {
+  uint64_t* d = nullptr;
+  TG_CUDA(cudaMalloc(&d, 8 * std::max<uint64_t>(n, 1)));
+  cudaError_t e = tg::probe_rng(seed, p, n, d, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(out, d, 8 * n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "probe_rng");
+  return TG_OK;
+}
+
+tg_status tg_probe_gates(uint32_t spins, uint64_t seed, uint64_t p, uint64_t steps,
+                         int initial_state, uint8_t* sites, double* u, double* uacc) {
+  if (spins < 2 || spins > 30) return fail(TG_ECONFIG, "spins out of range [2,30]: " + std::to_string(spins));
+  char* d = nullptr;
+  const size_t n = std::max<uint64_t>(steps, 1);
+  TG_CUDA(cudaMalloc(&d, n * (1 + 32 * 8 + 8) + 512));
+  double* du = reinterpret_cast<double*>(d);
+  double* da = du + 32 * n;
+  uint8_t* ds = reinterpret_cast<uint8_t*>(da + n);
+  cudaError_t e = tg::probe_gates(spins, seed, p, steps, initial_state, ds, du, da, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(sites, ds, steps, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(u, du, 8 * 32 * steps, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(uacc, da, 8 * steps, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "probe_gates");
+  return TG_OK;
+}
+
+tg_status tg_probe_apply_gate(uint32_t spins, const double* psi, int site, const double* u,
+                              double* out) {
+  if (spins < 2 || spins > 24) return fail(TG_EINVAL, "probe_apply_gate: spins must be in [2,24]");
+  if (site < 0 || static_cast<uint32_t>(site) + 2 > spins)
+    return fail(TG_EINVAL, "apply_two_site_gate: site " + std::to_string(site) + " out of range [0," +
+                               std::to_string(spins - 2) + "]");
+  const size_t n = size_t{1} << spins;
+  double* d = nullptr;
+  TG_CUDA(cudaMalloc(&d, 8 * (4 * n + 32)));
+  double *dp = d, *dout = d + 2 * n, *du = d + 4 * n;
+  cudaError_t e = cudaMemcpy(dp, psi, 16 * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(du, u, 256, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = tg::probe_apply_gate(spins, dp, site, du, dout, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, 16 * n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "probe_apply_gate");
+  return TG_OK;
+}
+
+tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* entropy,
+                           double* norms) {
+  if (spins < 2 || spins > 24) return fail(TG_EINVAL, "probe_entropy: spins must be in [2,24]");
+  if (count < 1) return TG_OK;
+  const size_t n = size_t{1} << spins;
+  double* d = nullptr;
+  TG_CUDA(cudaMalloc(&d, 8 * (2 * n * count + 2 * count)));
+  double *dp = d, *de = d + 2 * n * count, *dn = de + count;
+  cudaError_t e = cudaMemcpy(dp, psi, 16 * n * count, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = tg::probe_entropy(spins, count, dp, de, dn, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(entropy, de, 8 * count, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && norms) e = cudaMemcpy(norms, dn, 8 * count, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "probe_entropy");
+  return TG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,231 @@
+// tg_device.cuh — device building blocks of the persistent annealing kernels (sm_100a).
+//
+//  * xoshiro256++ / splitmix64 seeding: bit-exact port of rng.cpp:12-59 (integer work).
+//  * Box-Muller (rng.cpp:61-67) with CUDA libm log/sqrt/sincos (<= 2 ulp vs glibc).
+//  * Haar 4x4 unitary (spinmc.cpp:65-89): Ginibre fill + modified Gram-Schmidt, run by
+//    the producer warp, 4 lanes = 4 rows, unfused rounding (__dmul_rn/__dadd_rn) so that
+//    for identical G the result is bitwise the reference's.
+//  * mbarrier ring protocol between the producer warp and the consumer warps.
+//  * FP64 tensor op: mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4 (the only FP64 MMA shape on
+//    sm_100a; there is no tcgen05 kind for f64).
+#pragma once
+#include <cstdint>
+
+namespace tg {
+
+// ------------------------------------------------------------------------------ RNG
+struct Xoshiro {
+  uint64_t s0, s1, s2, s3;
+};
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// rng.cpp:23-33
+__host__ __device__ __forceinline__ Xoshiro stream_init(uint64_t global_seed, uint64_t p) {
+  uint64_t s = global_seed ^ mix64(p + 1);
+  uint64_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    s += 0x9E3779B97F4A7C15ULL;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    w[i] = z ^ (z >> 31);
+  }
+  if ((w[0] | w[1] | w[2] | w[3]) == 0) w[0] = 1;
+  return Xoshiro{w[0], w[1], w[2], w[3]};
+}
+
+__host__ __device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) {
+  return (x << k) | (x >> (64 - k));
+}
+
+// rng.cpp:35-45
+__host__ __device__ __forceinline__ uint64_t next_u64(Xoshiro& st) {
+  const uint64_t result = rotl64(st.s0 + st.s3, 23) + st.s0;
+  const uint64_t t = st.s1 << 17;
+  st.s2 ^= st.s0;
+  st.s3 ^= st.s1;
+  st.s1 ^= st.s2;
+  st.s0 ^= st.s3;
+  st.s2 ^= t;
+  st.s3 = rotl64(st.s3, 45);
+  return result;
+}
+
+// rng.cpp:47-49 (exact: a 53-bit integer converts exactly)
+__device__ __forceinline__ double u01(uint64_t x) {
+  return __dmul_rn(__ull2double_rn(x >> 11), 0x1.0p-53);
+}
+
+// rng.cpp:51-59: reject x < 2^64 mod n, return x mod n. Warp-uniform when all lanes
+// hold the same state.
+__device__ __forceinline__ uint32_t uniform_index(Xoshiro& st, uint64_t n) {
+  const uint64_t reject_below = (0 - n) % n;
+  for (;;) {
+    const uint64_t x = next_u64(st);
+    if (x >= reject_below) return static_cast<uint32_t>(x % n);
+  }
+}
+
+// rng.cpp:61-67 for the two draws (x1 -> u1, x2 -> u2).
+__device__ __forceinline__ void box_muller(uint64_t x1, uint64_t x2, double& a, double& b) {
+  const double u1 = __dsub_rn(1.0, u01(x1));
+  const double u2 = u01(x2);
+  const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+  const double angle = __dmul_rn(6.283185307179586, u2);  // (2.0 * std::numbers::pi) * u2
+  double s, c;
+  sincos(angle, &s, &c);
+  a = __dmul_rn(r, c);
+  b = __dmul_rn(r, s);
+}
+
+// ------------------------------------------------------------------- gate ring slot
+// One Metropolis proposal, data-independent of the trajectory: the
+// producer warp writes it steps ahead of the consumers.
+struct GateSlot {
+  double ur[16];   // U(x,y).re at x*4+y  (row-major: x = output basis index)
+  double ui[16];
+  double uacc;     // uniform01 acceptance draw (spinmc.cpp:207)
+  double temp;     // temperature(step)           (spinmc.cpp:178-184)
+  int32_t site;    // uniform_index(S-1)          (spinmc.cpp:198)
+  int32_t pad;
+};
+
+// Producer: generate the gate of one step. All 32 lanes hold the SAME xoshiro state and
+// advance it identically (34 draws), so control flow is warp-uniform. Lanes 0..15 each
+// produce one normal pair (element (k&3, k>>2) of G, column-major fill spinmc.cpp:68-73);
+// lanes 0..3 then run MGS as the 4 rows. Writes the slot (lanes 0..3) — caller fences.
+__device__ __forceinline__ void produce_gate(Xoshiro& st, int lane, uint32_t spins,
+                                             GateSlot* slot, double temp) {
+  const uint32_t site = uniform_index(st, static_cast<uint64_t>(spins - 1));
+  uint64_t d1 = 0, d2 = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const uint64_t x = next_u64(st);
+    if (j == 2 * lane) d1 = x;
+    if (j == 2 * lane + 1) d2 = x;
+  }
+  const uint64_t dacc = next_u64(st);
+  double gr = 0.0, gi = 0.0;
+  if (lane < 16) box_muller(d1, d2, gr, gi);
+  // lane i (0..3) gathers row i: q(i,j) lives on lane i + 4j.
+  const int row = lane & 3;
+  double qr[4], qi[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    qr[j] = __shfl_sync(0xffffffffu, gr, row + 4 * j);
+    qi[j] = __shfl_sync(0xffffffffu, gi, row + 4 * j);
+  }
+  // Modified Gram-Schmidt, spinmc.cpp:77-87, reductions over i in ascending order.
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int prev = 0; prev < j; ++prev) {
+      // term_i = conj(q(i,prev)) * q(i,j) = (ar*br - ai*bi, ar*bi + ai*br), ai = -q.im
+      const double ar = qr[prev], ai = -qi[prev];
+      const double tr = __dsub_rn(__dmul_rn(ar, qr[j]), __dmul_rn(ai, qi[j]));
+      const double ti = __dadd_rn(__dmul_rn(ar, qi[j]), __dmul_rn(ai, qr[j]));
+      double pr = 0.0, pi = 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        pr = __dadd_rn(pr, __shfl_sync(0xffffffffu, tr, i));
+        pi = __dadd_rn(pi, __shfl_sync(0xffffffffu, ti, i));
+      }
+      // q(i,j) -= proj * q(i,prev)
+      const double sr = __dsub_rn(__dmul_rn(pr, qr[prev]), __dmul_rn(pi, qi[prev]));
+      const double si = __dadd_rn(__dmul_rn(pr, qi[prev]), __dmul_rn(pi, qr[prev]));
+      qr[j] = __dsub_rn(qr[j], sr);
+      qi[j] = __dsub_rn(qi[j], si);
+    }
+    const double t = __dadd_rn(__dmul_rn(qr[j], qr[j]), __dmul_rn(qi[j], qi[j]));
+    double nrm = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) nrm = __dadd_rn(nrm, __shfl_sync(0xffffffffu, t, i));
+    nrm = __dsqrt_rn(nrm);
+    qr[j] = __ddiv_rn(qr[j], nrm);
+    qi[j] = __ddiv_rn(qi[j], nrm);
+  }
+  if (lane < 4) {
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      slot->ur[lane * 4 + y] = qr[y];
+      slot->ui[lane * 4 + y] = qi[y];
+    }
+  }
+  if (lane == 0) {
+    slot->site = static_cast<int32_t>(site);
+    slot->uacc = u01(dacc);
+    slot->temp = temp;
+  }
+}
+
+// spinmc.cpp:178-184 (producer-side: the schedule is data-independent)
+__device__ __forceinline__ double temperature(double t0, double t_min, uint64_t step,
+                                              uint64_t total) {
+  const double frac = __ddiv_rn(static_cast<double>(step), static_cast<double>(total));
+  return __dmul_rn(t0, pow(__ddiv_rn(t_min, t0), frac));
+}
+
+// spinmc.cpp:186-191
+__device__ __forceinline__ double acceptance(double delta, double t) {
+  double x = __ddiv_rn(delta, t);
+  x = (0.0 < x) ? 0.0 : x;
+  x = (x < -745.0) ? -745.0 : x;
+  return exp(x);
+}
+
+// ---------------------------------------------------------------------- mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Named barrier over the consumer warps only (id 1; the producer warp never joins).
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// -------------------------------------------------------------------------- DMMA
+// D = A*B + C, m8n8k4 f64. Lane l: A[l>>2][l&3], B[l&3][l>>2], C/D[l>>2][2(l&3)+{0,1}].
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int64_t globaltimer() {
+  int64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace tg

@@ -1,0 +1,58 @@
+// tg_internal.h — launch interface between the C-ABI host layer (capi.cpp) and the
+// CUDA translation units. Not part of the public boundary (include/taskgemm_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tg {
+
+// Everything one persistent anneal launch needs. Rows r in [0, rows) are replicas
+// p = p_first + r * p_stride (p mod devices / shard binding, bench.cpp:171).
+struct AnnealParams {
+  uint32_t spins;
+  int32_t objective;      // 0 maximize, 1 minimize
+  int32_t initial_state;  // 0 product, 1 random
+  int32_t inject_fault;
+  uint64_t steps, seed, renorm;
+  double t0, t_min;
+  uint64_t rows, p_first, p_stride;
+  double* initial_entropy;
+  double* entropies;
+  uint8_t* accepted;
+  uint8_t* sites;
+  int64_t* wall_ns;
+  double* final_entropy;
+  int32_t* status;
+  int64_t* status_step;
+  double* workspace;  // HBM tier: per-CTA psi/psi' slabs
+};
+
+// Status codes written per row by the kernels.
+enum : int32_t { kRowOk = 0, kRowNotNormalized = 2 };
+
+constexpr int kSmemMaxSpins = 12;
+
+// anneal_smem.cu (S <= 12)
+cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* grid_out);
+// anneal_hbm.cu (S >= 13)
+cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out);
+size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device);
+
+// probes.cu
+cudaError_t probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* d_out, cudaStream_t s);
+cudaError_t probe_gates(uint32_t spins, uint64_t seed, uint64_t p, uint64_t steps, int initial,
+                        uint8_t* d_sites, double* d_u, double* d_uacc, cudaStream_t s);
+cudaError_t probe_apply_gate(uint32_t spins, const double* d_psi, int site, const double* d_u,
+                             double* d_out, cudaStream_t s);
+cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* d_psi, double* d_e,
+                          double* d_norm, cudaStream_t s);
+cudaError_t fp64_dmma_peak(double* tflops, double* clock_ghz);
+
+// zgemm.cu
+cudaError_t launch_zgemm_strided(int batch, int m, int n, int k, double ar, double ai,
+                                 const double* A, int64_t sA, const double* B, int64_t sB,
+                                 double br, double bi, const double* C, int64_t sC, double* out,
+                                 int64_t sO, int inject_fault, cudaStream_t stream);
+
+}  // namespace tg

@@ -78,6 +78,10 @@ class Oracle:
         L.tgo_next_u64.argtypes = [C.c_void_p]
         L.tgo_next_u64.restype = C.c_uint64
         L.tgo_haar.argtypes = [C.c_void_p, _dp]
+        L.tgo_uniform_index.argtypes = [C.c_void_p, C.c_uint64]
+        L.tgo_uniform_index.restype = C.c_uint64
+        L.tgo_uniform01.argtypes = [C.c_void_p]
+        L.tgo_uniform01.restype = C.c_double
         L.tgo_apply_gate.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp]
         L.tgo_gemm.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]
         L.tgo_entropy.argtypes = [C.c_int, _dp, C.c_int, _dp]
@@ -104,6 +108,22 @@ class Oracle:
             row = np.zeros(32)
             self.L.tgo_haar(st, _ptr(row, _dp))
             out[i] = row
+        return out
+
+    def haar_stream(self, spins: int, seed: int, p: int, steps: int, random_start: bool) -> np.ndarray:
+        """The Haar unitaries of steps 0..steps-1 of replica p (draw order of spinmc.cpp:229-232,198-207)."""
+        st = (C.c_uint64 * 4)()
+        self.L.tgo_stream_init(st, seed, p)
+        if random_start:
+            for _ in range(2 << spins):
+                self.L.tgo_next_u64(st)
+        out = np.zeros((steps, 32))
+        for i in range(steps):
+            self.L.tgo_uniform_index(st, spins - 1)
+            row = np.zeros(32)
+            self.L.tgo_haar(st, _ptr(row, _dp))
+            out[i] = row
+            self.L.tgo_uniform01(st)
         return out
 
     def apply_gate(self, spins: int, psi: np.ndarray, site: int, u: np.ndarray) -> np.ndarray:

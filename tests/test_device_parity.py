@@ -1,0 +1,237 @@
+"""GPU parity suite: the CUDA path through the C ABI against the
+oracle / the reference's golden outputs. Integer work (RNG words, sites, accept flags) is
+bit-exact; floating point within the north-star tolerance |got-want| <= 1e-10*max(|want|,1)
+(SURVEY fact 8). Run on a B200: `python -m pytest tests -m gpu`."""
+import math
+
+import numpy as np
+import pytest
+from conftest import TRAJ_CASES, load_traj
+from oracle_lib import McCfg
+
+import paper_2203_09353_b200 as tg
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def close(got, want, tol=TOL):
+    got, want = np.asarray(got), np.asarray(want)
+    return np.abs(got - want) <= tol * np.maximum(np.abs(want), 1.0)
+
+
+# ---------------------------------------------------------------- T1/T2 RNG and gates
+@pytest.mark.parametrize("seed", [0, 1, 42, 2**64 - 1])
+@pytest.mark.parametrize("p", [0, 1, 7, 65535])
+def test_t1_device_xoshiro_bitwise(kats, oracle, seed, p):
+    got = tg.probe_rng(seed, p, 10000)
+    assert np.array_equal(got, oracle.first_u64(seed, p, 10000))
+    idx = [i for i, (s, q) in enumerate(kats["u64_pairs"]) if int(s) == seed and int(q) == p][0]
+    assert np.array_equal(got[:256], kats["u64"][idx])
+
+
+@pytest.mark.parametrize("spins,initial", [(8, "product"), (2, "product"), (13, "product"), (6, "random")])
+def test_t2_t3_gate_stream(oracle, spins, initial):
+    """Sites bit-exact, Haar U within a few ulp of the reference, u_accept bit-exact."""
+    steps = 300
+    sites, u, ua = tg.probe_gates(spins, 11, 5, steps, initial)
+    _, _, _, osites, ou, _ = oracle.mc_procedure(
+        McCfg(spins=spins, steps=steps, seed=11, initial_state=1 if initial == "random" else 0), 5)
+    assert np.array_equal(sites, osites)
+    assert np.array_equal(ua, ou)
+    # Haar matrices: replay the stream on the oracle side
+    st_u = oracle.haar_stream(spins, 11, 5, steps, initial == "random")
+    ulp = np.abs(u - st_u) / np.spacing(np.maximum(np.abs(st_u), 1e-300))
+    assert np.abs(u - st_u).max() <= 1e-14
+    us = u.view(np.complex128).reshape(-1, 4, 4).transpose(0, 2, 1)
+    gram = np.einsum("nki,nkj->nij", us.conj(), us) - np.eye(4)
+    assert np.abs(gram).max() <= 1e-12
+    assert np.median(ulp) <= 4
+
+
+# ------------------------------------------------------------------- T4 gate application
+def test_t4_gate_bitwise(kats):
+    for i in range(int(kats["n_gates"])):
+        spins, site = (int(x) for x in kats[f"gate{i}_meta"])
+        got = tg.probe_apply_gate(spins, kats[f"gate{i}_in"], site, kats[f"gate{i}_u"])
+        want = kats[f"gate{i}_out"]
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (spins, site)
+
+
+@pytest.mark.parametrize("spins", [14, 16])
+def test_t4_gate_bitwise_hbm(oracle, spins):
+    rng = np.random.default_rng(spins)
+    psi = rng.standard_normal(1 << spins) + 1j * rng.standard_normal(1 << spins)
+    psi /= np.linalg.norm(psi)
+    u = oracle.haar(3, spins, 1)[0].view(np.complex128)
+    for site in (0, 1, spins // 2 - 1, spins - 2):
+        got = tg.probe_apply_gate(spins, psi, site, u)
+        want = oracle.apply_gate(spins, psi, site, u)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), site
+
+
+# ---------------------------------------------------------------- T5 GEMM (rho and batched)
+@pytest.mark.parametrize("spins", [2, 3, 4, 6, 8, 9, 12, 13, 14])
+def test_t5_rho_entropy_vs_reference(kats, spins):
+    states = kats[f"ent_{spins}_states"]
+    e, n = tg.probe_entropy(spins, states)
+    assert close(e, kats[f"ent_{spins}_renyi2"]).all()
+    assert np.abs(n - 1.0).max() <= 1e-13
+
+
+@pytest.mark.parametrize("spins", [16, 18])
+def test_t5_rho_entropy_large(oracle, spins):
+    rng = np.random.default_rng(100 + spins)
+    psi = rng.standard_normal(1 << spins) + 1j * rng.standard_normal(1 << spins)
+    psi /= np.linalg.norm(psi)
+    e, n = tg.probe_entropy(spins, psi[None])
+    # numpy reference for the Frobenius norm of rho (the oracle's O(d^3) loop is slow at S=18)
+    da = 1 << (spins // 2)
+    Psi = psi.reshape(-1, da).T
+    rho = Psi @ Psi.conj().T
+    want = -math.log(np.sum(np.abs(rho) ** 2))
+    assert close(e, [max(want, 0.0)], 1e-11).all()
+    if spins == 16:
+        assert close(e, [oracle.entropy(spins, psi, 1)]).all()
+
+
+def test_t5_batched_gemm_vs_reference(device, kats):
+    for i in range(40):
+        a, b, c = kats[f"g{i}_a"], kats[f"g{i}_b"], kats[f"g{i}_c"]
+        al, be = kats[f"g{i}_ab"]
+        (out,), recs = device.batched_gemm([a], [b], [c], alpha=al, beta=be, records=True)
+        want = kats[f"g{i}_out"]
+        err = np.abs(out - want).max() / np.abs(want).max()
+        assert err <= 1e-13, (i, err)
+        assert recs[0].flops == 8 * a.shape[0] * b.shape[1] * a.shape[1]
+
+
+def test_t5_batched_gemm_ordered_and_large(device, oracle):
+    rng = np.random.default_rng(7)
+    for (m, n, k, batch) in [(64, 64, 64, 17), (100, 37, 130, 5), (256, 256, 256, 3), (1, 1, 1, 4)]:
+        As = [rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k)) for _ in range(batch)]
+        Bs = [rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n)) for _ in range(batch)]
+        outs, recs = device.batched_gemm(As, Bs, records=True, procedures=list(range(100, 100 + batch)))
+        for i in range(batch):
+            want = As[i] @ Bs[i]
+            assert np.abs(outs[i] - want).max() <= 1e-13 * max(1.0, np.abs(want).max()) * max(1, k)
+        assert [r.procedure for r in recs] == list(range(100, 100 + batch))
+    with pytest.raises(ValueError, match="fixed-size"):
+        device.batched_gemm([np.eye(2), np.eye(3)], [np.eye(2), np.eye(3)])
+
+
+# -------------------------------------------------------------------- T6 analytic states
+def test_t6_analytic_entropies():
+    for spins in (4, 6, 8, 12, 14):
+        prod = np.zeros(1 << spins, complex)
+        prod[0] = 1
+        ghz = np.zeros(1 << spins, complex)
+        ghz[0] = ghz[-1] = 1 / math.sqrt(2)
+        # Bell pairs across the cut: floor(S/2) ... use one Bell pair (sites 0 and S/2): ln 2
+        e, _ = tg.probe_entropy(spins, np.stack([prod, ghz]))
+        assert abs(e[0]) <= 1e-10
+        assert abs(e[1] - math.log(2)) <= 1e-10
+
+
+# ------------------------------------------------------------ T7 trajectories vs reference
+def cfg_from(g, procedures=None):
+    return tg.ExperimentConfig(
+        spins=int(g["spins"]), steps=int(g["steps"]), procedures=procedures or int(g["procedures"]),
+        seed=int(g["seed"]), objective="max" if int(g["objective"]) == 0 else "min",
+        initial_state="product" if int(g["initial_state"]) == 0 else "random",
+        t0=float(g["t0"]), t_min=float(g["t_min"]), renormalize_interval=int(g["renorm"]))
+
+
+def assert_traj_parity(rep, g, rows=None):
+    rows = rows if rows is not None else slice(None)
+    assert np.array_equal(rep.sites, g["sites"][rows]), "site sequence differs"
+    mism = np.argwhere(rep.accepted != g["accepted"][rows])
+    assert mism.size == 0, f"accept flags differ at {mism[:5].tolist()}"
+    ok = close(rep.entropies, g["entropies"][rows])
+    assert ok.all(), f"max scaled diff {np.max(np.abs(rep.entropies - g['entropies'][rows]))}"
+    assert close(rep.initial_entropy, g["initial"][rows]).all()
+
+
+@pytest.mark.parametrize("name", TRAJ_CASES)
+def test_t7_trajectory_parity(device, name):
+    g = load_traj(name)
+    rep = device.run(cfg_from(g))
+    assert_traj_parity(rep, g)
+    assert abs(rep.average_entropy - float(g["average"])) <= TOL * max(1.0, abs(float(g["average"])))
+    assert rep.total_flops == (rep.entropies.size + rep.initial_entropy.size) * tg.step_flops(int(g["spins"]))
+
+
+def test_t7_config1_appendix_a(device):
+    g = load_traj("cfg1")
+    rep = device.run(cfg_from(g))
+    assert int(rep.accepted.sum()) == 59437
+    assert list(rep.sites[0, :12]) == [0, 1, 5, 6, 2, 2, 0, 5, 4, 2, 0, 2]
+    assert abs(rep.average_entropy - 2.2063680065173292) <= 1e-10 * 2.21
+
+
+@pytest.mark.slow
+def test_t7_config2_subset_full_length(device, oracle):
+    """BASELINE configs[1] (S=12, 1024 replicas, 10k steps) on the device; the oracle checks
+    a bounded subset of replicas over the full 10k steps; all rows obey the invariants."""
+    cfg = tg.ExperimentConfig(spins=12, steps=10000, procedures=1024)
+    rep = device.run(cfg)
+    sub = list(range(0, 1024, 128))
+    ocfg = McCfg(spins=12, steps=10000)
+    for p in sub:
+        init, ent, acc, sites, _, _ = oracle.mc_procedure(ocfg, p)
+        assert np.array_equal(rep.sites[p], sites)
+        assert np.array_equal(rep.accepted[p], acc), p
+        assert close(rep.entropies[p], ent).all()
+    assert (rep.sites < 11).all()
+    assert (rep.entropies >= 0).all() and (rep.entropies <= 6 * math.log(2) + 1e-9).all()
+    fin = rep.entropies[:, -1]
+    assert rep.average_entropy == pytest.approx(float(np.mean(fin)), rel=1e-12)
+
+
+# -------------------------------------------------------------- T8 determinism / sharding
+def test_t8_rerun_bitwise_and_shards(device):
+    cfg = tg.ExperimentConfig(spins=10, steps=300, procedures=37, seed=99)
+    a = device.run(cfg)
+    b = device.run(cfg)
+    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
+    assert np.array_equal(a.accepted, b.accepted)
+    # shard (rank 1 of 3) sees exactly replicas 1, 4, 7, ... with identical traces
+    cfg3 = tg.ExperimentConfig(spins=10, steps=300, procedures=37, seed=99, shard_index=1, shard_count=3)
+    s = device.run(cfg3)
+    assert np.array_equal(s.procedures, np.arange(1, 37, 3))
+    assert np.array_equal(s.entropies.view(np.uint64), a.entropies[1::3].view(np.uint64))
+
+
+def test_t8_hbm_tier_rerun_bitwise(device):
+    cfg = tg.ExperimentConfig(spins=14, steps=20, procedures=5, seed=3)
+    a = device.run(cfg)
+    b = device.run(cfg)
+    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
+
+
+# ------------------------------------------------------------------------ T9 error paths
+def test_t9_fault_injection_detected(device):
+    g = load_traj("s12")
+    cfg = cfg_from(g)
+    cfg.inject_fault = True
+    rep = device.run(cfg)
+    assert not close(rep.initial_entropy, g["initial"]).all() or not close(rep.entropies, g["entropies"]).all()
+
+
+def test_t9_shutdown_and_config_errors():
+    dev = tg.Device([0])
+    dev.shutdown()
+    with pytest.raises(tg.SubmissionError):
+        dev.run(tg.ExperimentConfig(spins=4, steps=2, procedures=1))
+    dev.close()
+    with pytest.raises(tg.ConfigError, match=r"spins out of range \[2,30\]"):
+        tg.run_experiment(tg.ExperimentConfig(spins=31))
+    with pytest.raises(tg.ConfigError):
+        tg.Device([0]).run(tg.ExperimentConfig(spins=4, devices=2))
+
+
+def test_zero_steps_and_single_replica(device):
+    rep = device.run(tg.ExperimentConfig(spins=8, steps=0, procedures=3))
+    assert rep.entropies.shape == (3, 0)
+    assert np.all(np.abs(rep.initial_entropy) <= 1e-15)
+    assert rep.average_entropy == pytest.approx(float(np.mean(rep.initial_entropy)), abs=1e-15)
