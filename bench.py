@@ -310,8 +310,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded product states, seed 0)",
-            "config": {"workload": cfgw["name"], "spins": spins, "gemm_mnk": list(tg.dims_for_spins(spins)[:1] * 2
-                       + [tg.dims_for_spins(spins)[1]]), "replicas_per_gpu": R, "procedures": procedures,
+            "config": {"workload": cfgw["name"], "spins": spins, "gemm_mnk": [tg.dims_for_spins(spins)[0]] * 2 + [tg.dims_for_spins(spins)[1]], "replicas_per_gpu": R, "procedures": procedures,
                        "mc_steps": S, "parallelism": f"dp{world} (replica p on GPU p mod {world})",
                        "entropy": "renyi-2", "l2": "flushed between timed iterations (256 MiB write)"},
             "tflops": replica_steps * tg.step_flops(spins) / t_step / 1e12,
