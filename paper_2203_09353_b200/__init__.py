@@ -100,7 +100,7 @@ EXPORTS = [
     "tg_anneal_rows", "tg_step_flops", "tg_anneal_run", "tg_anneal_launch",
     "tg_anneal_workspace_bytes", "tg_zgemm_batched", "tg_zgemm_strided_launch",
     "tg_fp64_dmma_peak", "tg_probe_rng", "tg_probe_gates", "tg_probe_apply_gate",
-    "tg_probe_entropy",
+    "tg_probe_entropy", "tg_probe_phase_trace",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -142,6 +142,7 @@ def lib() -> C.CDLL:
     L.tg_probe_gates.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _u8p, _dp, _dp]
     L.tg_probe_apply_gate.argtypes = [C.c_uint32, _dp, C.c_int, _dp, _dp]
     L.tg_probe_entropy.argtypes = [C.c_uint32, C.c_uint64, _dp, _dp, _dp]
+    L.tg_probe_phase_trace.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64)]
     for name in EXPORTS:
         if name not in ("tg_last_error", "tg_version", "tg_anneal_rows", "tg_step_flops",
                         "tg_anneal_workspace_bytes"):
@@ -410,6 +411,13 @@ def probe_entropy(spins: int, states: np.ndarray):
     _check(lib().tg_probe_entropy(spins, states.shape[0], states.ctypes.data_as(_dp), e.ctypes.data_as(_dp),
                                   n.ctypes.data_as(_dp)))
     return e, n
+
+
+def probe_phase_trace(spins: int, replicas: int, steps: int) -> np.ndarray:
+    """clock64 phase stamps [steps, 8] of CTA 0's first replica (profiling only)."""
+    out = np.zeros((steps, 8), np.int64)
+    _check(lib().tg_probe_phase_trace(spins, replicas, steps, out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out
 
 
 def fp64_dmma_peak(device: int = 0) -> tuple[float, float]:

@@ -7,24 +7,6 @@
 namespace tg {
 namespace hbm {
 
-__device__ void fill_random(const Geo& G, Xoshiro& st, int lane, double* X, double* Y) {
-  for (int c = 0; c < G.n / 16; ++c) {
-    uint64_t d1 = 0, d2 = 0;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const uint64_t x = next_u64(st);
-      if (j == 2 * lane) d1 = x;
-      if (j == 2 * lane + 1) d2 = x;
-    }
-    if (lane < 16) {
-      double a, b;
-      box_muller(d1, d2, a, b);
-      X[c * 16 + lane] = a;
-      Y[c * 16 + lane] = b;
-    }
-  }
-}
-
 __device__ void renormalize(const Geo& G, double* X, double* Y, int tid, int warp, int lane,
                             Header& H) {
   double s = 0.0;
@@ -54,51 +36,26 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   double* stages = reinterpret_cast<double*>(smem_raw + kHeaderBytes);
   const Geo G(static_cast<int>(P.spins));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool producer = warp == kConsumerWarps;
   double* slab = P.workspace + static_cast<size_t>(blockIdx.x) * 4 * G.n;
   auto PX = [&](int b) { return slab + (2 * b) * static_cast<size_t>(G.n); };
   auto PY = [&](int b) { return slab + (2 * b + 1) * static_cast<size_t>(G.n); };
 
-  if (tid == 0) {
-    for (int i = 0; i < kRing; ++i) {
-      mbar_init(&H.full[i], 1);
-      mbar_init(&H.empty[i], 1);
-    }
-  }
-  __syncthreads();
-
-  uint64_t gseq = 0;
   for (uint64_t r = blockIdx.x; r < P.rows; r += gridDim.x) {
-    const uint64_t p = P.p_first + r * P.p_stride;
-    if (producer) {
-      Xoshiro st = stream_init(P.seed, p);
-      __syncthreads();  // A
-      if (P.initial_state == 1) {
-        fill_random(G, st, lane, PX(0), PY(0));
-        __threadfence_block();
-      }
-      __syncthreads();  // B
-      for (uint64_t s = 0; s < P.steps; ++s, ++gseq) {
-        const int slot = static_cast<int>(gseq % kRing);
-        const uint32_t par = static_cast<uint32_t>((gseq / kRing) & 1);
-        mbar_wait(&H.empty[slot], par ^ 1u);
-        const double temp = temperature(P.t0, P.t_min, s, P.steps);
-        produce_gate(st, lane, G.spins, &H.ring[slot], temp);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&H.full[slot]);
-      }
-      continue;
-    }
-
+    const GateRec* recs = P.gates + r * P.steps;
     if (P.initial_state == 0) {
-      for (int i = tid; i < G.n; i += kConsumers) {
+      for (int i = tid; i < G.n; i += kConsumers) {  // product_state (spinmc.cpp:28-35)
         __stcg(PX(0) + i, i == 0 ? 1.0 : 0.0);
         __stcg(PY(0) + i, 0.0);
       }
-      __threadfence_block();
+    } else {  // random_state (spinmc.cpp:37-48), normals from the pre-pass
+      const double* src = P.init_states + r * 2 * static_cast<size_t>(G.n);
+      for (int i = tid; i < G.n; i += kConsumers) {
+        __stcg(PX(0) + i, src[2 * i]);
+        __stcg(PY(0) + i, src[2 * i + 1]);
+      }
     }
-    __syncthreads();  // A
-    __syncthreads();  // B
+    __threadfence_block();
+    __syncthreads();
     int cur = 0;
     if (P.initial_state == 1) renormalize(G, PX(0), PY(0), tid, warp, lane, H);
 
@@ -131,23 +88,13 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     consumer_sync(kConsumers);
     bool err = H.error != 0;
 
-    for (uint64_t s = 0; s < P.steps; ++s, ++gseq) {
-      const int slot = static_cast<int>(gseq % kRing);
-      const uint32_t par = static_cast<uint32_t>((gseq / kRing) & 1);
-      mbar_wait(&H.full[slot], par);
-      const GateSlot& g = H.ring[slot];
-      if (err) {
-        if (tid == 0) mbar_arrive(&H.empty[slot]);
-        continue;
-      }
-      int64_t t_start = 0;
-      if (tid == 0 && P.wall_ns) t_start = globaltimer();
+    int64_t t_prev = (tid == 0 && P.wall_ns) ? globaltimer() : 0;
+    for (uint64_t s = 0; s < P.steps && !err; ++s) {
+      const GateRec& g = recs[s];
       const int site = g.site;
-      const double uacc = g.uacc, temp = g.temp;
       gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), G.spins, site, g, tid, kConsumers);
       __threadfence_block();
       consumer_sync(kConsumers);
-      if (tid == 0) mbar_arrive(&H.empty[slot]);
       rho_partials(G, PX(cur ^ 1), PY(cur ^ 1), stages, tid, warp, lane, P.inject_fault != 0,
                    rho2, tr);
       if (lane == 0) {
@@ -170,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
         } else {
           const double proposed = smem::renyi2(a);
           const double delta = P.objective == 0 ? proposed - cur_e : cur_e - proposed;
-          acc = uacc < acceptance(delta, temp);
+          acc = g.u < acceptance(delta, g.temp);
           if (acc) cur_e = proposed;
         }
         H.decision = acc;
@@ -178,7 +125,11 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
         P.entropies[o] = cur_e;
         P.accepted[o] = static_cast<uint8_t>(acc);
         if (P.sites) P.sites[o] = static_cast<uint8_t>(site);
-        if (P.wall_ns) P.wall_ns[o] = globaltimer() - t_start;
+        if (P.wall_ns) {
+          const int64_t t_now = globaltimer();
+          P.wall_ns[o] = t_now - t_prev;
+          t_prev = t_now;
+        }
       }
       consumer_sync(kConsumers);
       err = H.error != 0;
@@ -187,13 +138,14 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
         renormalize(G, PX(cur), PY(cur), tid, warp, lane, H);
     }
     if (tid == 0 && P.final_entropy) P.final_entropy[r] = cur_e;
+    __syncthreads();  // the slab is rewritten by the next replica
   }
 }
 
 // ----------------------------------------------------------------------------- probes
 __global__ void gate_probe_kernel(int spins, const double* psi, int site, const double* u,
                                   double* scratch, double* out) {
-  __shared__ GateSlot g;
+  __shared__ GateRec g;
   const int tid = threadIdx.x;
   const int n = 1 << spins;
   if (tid < 16) {

@@ -110,9 +110,60 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
   return p;
 }
 
-cudaError_t launch(const tg::AnnealParams& p, cudaStream_t s) {
-  return p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::launch_anneal_smem(p, s, nullptr)
-                                                            : tg::launch_anneal_hbm(p, s, nullptr);
+// Replicas per batch are capped so the pre-generated proposal stream (288 B per
+// replica-step + raw draws) stays within this many bytes of workspace.
+constexpr size_t kStreamBudget = size_t{16} << 30;
+
+size_t slab_bytes(uint32_t spins, uint64_t rows, int device) {
+  return spins > static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::anneal_hbm_workspace_bytes(spins, rows, device)
+                                                         : 0;
+}
+
+// Workspace for one launch: [proposal stream of one batch][HBM-tier slabs] (+ alignment).
+size_t workspace_for(const tg::AnnealParams& p, int device) {
+  const size_t per_row = tg::gate_stream_bytes_per_row(p.spins, p.steps, p.initial_state == 1);
+  const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(p.rows, kStreamBudget / per_row));
+  return batch * per_row + slab_bytes(p.spins, batch, device) + 1024;
+}
+
+// The whole device pipeline of one launch, on one stream: per batch of replicas, the
+// proposal-stream pre-pass (gate_stream.cu) then the persistent anneal kernel.
+cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStream_t s,
+                   bool trace = false) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (p.rows == 0) return cudaSuccess;
+  const size_t per_row = tg::gate_stream_bytes_per_row(p.spins, p.steps, p.initial_state == 1);
+  uint64_t batch = std::min<uint64_t>(p.rows, kStreamBudget / per_row);
+  while (batch > 0 && batch * per_row + slab_bytes(p.spins, batch, dev) + 1024 > ws_bytes) --batch;
+  if (batch == 0) return cudaErrorMemoryAllocation;
+  const size_t stream_bytes = batch * per_row;
+  char* base = static_cast<char*>(ws);
+  char* slabs = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(base + stream_bytes) + 255) & ~uintptr_t{255});
+  for (uint64_t b0 = 0; b0 < p.rows; b0 += batch) {
+    tg::AnnealParams q = p;
+    q.rows = std::min<uint64_t>(batch, p.rows - b0);
+    q.p_first = p.p_first + b0 * p.p_stride;
+    const uint64_t o = b0 * p.steps;
+    q.initial_entropy = p.initial_entropy + b0;
+    q.final_entropy = p.final_entropy ? p.final_entropy + b0 : nullptr;
+    q.status = p.status + b0;
+    q.status_step = p.status_step + b0;
+    q.entropies = p.entropies + o;
+    q.accepted = p.accepted + o;
+    q.sites = p.sites ? p.sites + o : nullptr;
+    q.wall_ns = p.wall_ns ? p.wall_ns + o : nullptr;
+    tg::GateStream gs{};
+    cudaError_t e = tg::launch_gate_stream(q, base, stream_bytes, &gs, s);
+    if (e != cudaSuccess) return e;
+    q.gates = gs.recs;
+    q.init_states = gs.init_states;
+    if (!trace) q.workspace = reinterpret_cast<double*>(slabs);
+    e = p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::launch_anneal_smem(q, s, nullptr, trace)
+                                                           : tg::launch_anneal_hbm(q, s, nullptr);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 template <class T>
@@ -194,10 +245,10 @@ tg_status tg_destroy(tg_ctx* ctx) {
 }
 
 size_t tg_anneal_workspace_bytes(const tg_anneal_config* cfg) {
-  if (!cfg || cfg->spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) || cfg->spins > 24) return 0;
+  if (!cfg || cfg->spins < 2 || cfg->spins > 24) return 0;
   int dev = 0;
   cudaGetDevice(&dev);
-  return tg::anneal_hbm_workspace_bytes(cfg->spins, rows_for(cfg), dev);
+  return workspace_for(make_params(cfg, rows_for(cfg), 0, 1), dev);
 }
 
 tg_status tg_anneal_launch(const tg_anneal_config* cfg, const tg_anneal_device_buffers* b,
@@ -217,10 +268,11 @@ tg_status tg_anneal_launch(const tg_anneal_config* cfg, const tg_anneal_device_b
   p.final_entropy = b->final_entropy;
   p.status = b->status;
   p.status_step = b->status_step;
-  p.workspace = static_cast<double*>(b->workspace);
-  if (cfg->spins > static_cast<uint32_t>(tg::kSmemMaxSpins) && !p.workspace)
-    return fail(TG_EINVAL, "workspace required for spins > 12 (tg_anneal_workspace_bytes)");
-  cudaError_t e = launch(p, static_cast<cudaStream_t>(stream));
+  if (!b->workspace && rows > 0)
+    return fail(TG_EINVAL, "workspace required (tg_anneal_workspace_bytes)");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = launch(p, b->workspace, workspace_for(p, dev), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "anneal launch");
   return TG_OK;
 }
@@ -281,19 +333,16 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
     p.accepted = carve<uint8_t>(cur, lrows * steps);
     p.sites = want_sites ? carve<uint8_t>(cur, lrows * steps) : nullptr;
     p.wall_ns = want_wall ? carve<int64_t>(cur, lrows * steps) : nullptr;
-    if (cfg->spins > static_cast<uint32_t>(tg::kSmemMaxSpins)) {
-      const size_t ws = tg::anneal_hbm_workspace_bytes(cfg->spins, lrows, d.ordinal);
-      if (ws > d.workspace_bytes) {
-        if (d.workspace) cudaFree(d.workspace);
-        d.workspace = nullptr;
-        d.workspace_bytes = 0;
-        if (!cu(cudaMalloc(&d.workspace, ws), "cudaMalloc(workspace)")) return;
-        d.workspace_bytes = ws;
-      }
-      p.workspace = static_cast<double*>(d.workspace);
+    const size_t ws = workspace_for(p, d.ordinal);
+    if (ws > d.workspace_bytes) {
+      if (d.workspace) cudaFree(d.workspace);
+      d.workspace = nullptr;
+      d.workspace_bytes = 0;
+      if (!cu(cudaMalloc(&d.workspace, ws), "cudaMalloc(workspace)")) return;
+      d.workspace_bytes = ws;
     }
     if (!cu(cudaEventRecord(d.ev0, d.stream), "cudaEventRecord")) return;
-    if (!cu(launch(p, d.stream), "anneal launch")) return;
+    if (!cu(launch(p, d.workspace, d.workspace_bytes, d.stream), "anneal launch")) return;
     if (!cu(cudaEventRecord(d.ev1, d.stream), "cudaEventRecord")) return;
     // copy back: rows of this GPU are host rows g + D*q
     std::vector<double> init(lrows), fin(lrows), ent(lrows * steps);
@@ -505,6 +554,47 @@ tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, do
   if (e == cudaSuccess && norms) e = cudaMemcpy(norms, dn, 8 * count, cudaMemcpyDeviceToHost);
   cudaFree(d);
   if (e != cudaSuccess) return cuda_fail(e, "probe_entropy");
+  return TG_OK;
+}
+
+tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* trace) {
+  if (spins < 2 || spins > static_cast<uint32_t>(tg::kSmemMaxSpins))
+    return fail(TG_EINVAL, "phase trace covers the SMEM tier (spins <= 12)");
+  tg_anneal_config c{};
+  c.spins = spins;
+  c.devices = 1;
+  c.steps = steps;
+  c.procedures = replicas;
+  c.entropy_kind = TG_RENYI2;
+  c.t0 = 1.0;
+  c.t_min = 1e-3;
+  c.renormalize_interval = 1000;
+  c.shard_count = 1;
+  tg::AnnealParams p = make_params(&c, replicas, 0, 1);
+  char* d = nullptr;
+  const size_t bytes = trace_bytes(replicas, steps, false, false) + 64 * std::max<uint64_t>(steps, 1);
+  TG_CUDA(cudaMalloc(&d, bytes));
+  char* cur = d;
+  p.initial_entropy = carve<double>(cur, replicas);
+  p.final_entropy = carve<double>(cur, replicas);
+  p.status = carve<int32_t>(cur, replicas);
+  p.status_step = carve<int64_t>(cur, replicas);
+  p.entropies = carve<double>(cur, replicas * steps);
+  p.accepted = carve<uint8_t>(cur, replicas * steps);
+  int64_t* tr = carve<int64_t>(cur, 8 * steps);
+  p.workspace = reinterpret_cast<double*>(tr);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t wsb = workspace_for(p, dev);
+  void* ws = nullptr;
+  cudaError_t e = cudaMalloc(&ws, wsb);
+  if (e == cudaSuccess) e = cudaMemset(tr, 0, 64 * steps);
+  if (e == cudaSuccess) e = launch(p, ws, wsb, nullptr, /*trace=*/true);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(trace, tr, 64 * steps, cudaMemcpyDeviceToHost);
+  cudaFree(ws);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "probe_phase_trace");
   return TG_OK;
 }
 

@@ -16,8 +16,7 @@ namespace hbm {
 
 constexpr int kConsumerWarps = smem::kConsumerWarps;
 constexpr int kConsumers = smem::kConsumers;
-constexpr int kThreads = smem::kThreads;
-constexpr int kRing = smem::kRing;
+constexpr int kThreads = smem::kConsumers;  // no producer warp: the stream is pre-generated
 constexpr int TB = 64;        // output tile (complex rows/cols)
 constexpr int KC = 32;        // K columns per pipeline stage
 constexpr int SP = TB + 4;    // SMEM pitch (doubles)
@@ -30,14 +29,6 @@ using smem::Header;
 constexpr int kHeaderBytes = smem::kHeaderBytes;
 constexpr int kSmemBytes = kHeaderBytes + kStages * kStage * 8;
 
-__device__ __forceinline__ void cp_async16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 struct Geo {
   int spins, la, da, db, n;
@@ -46,10 +37,12 @@ struct Geo {
   __device__ int kchunks() const { return db / KC; }
 };
 
-// Gate application (spinmc.cpp:91-136), global planar -> global planar, reference rounding.
+// Gate application (spinmc.cpp:91-136), global planar -> global planar, reference rounding
+// (bitwise the reference's psi' for the same U). R = GateRec (global or SMEM).
+template <class R>
 __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const double* __restrict__ sy,
                                           double* __restrict__ dx, double* __restrict__ dy,
-                                          int spins, int site, const GateSlot& g, int tid,
+                                          int spins, int site, const R& g, int tid,
                                           int nthreads) {
   double ur[16], ui[16];
 #pragma unroll

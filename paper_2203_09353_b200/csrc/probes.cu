@@ -13,32 +13,18 @@ __global__ void rng_kernel(uint64_t seed, uint64_t p, uint64_t n, uint64_t* out)
   for (uint64_t i = 0; i < n; ++i) out[i] = next_u64(st);
 }
 
-// One warp = the producer of one replica: replays the draw order of mc_procedure
-// (random start consumes 2^S normal pairs first) and emits `steps` gates.
-__global__ void gates_kernel(uint32_t spins, uint64_t seed, uint64_t p, uint64_t steps,
-                             int initial, uint8_t* sites, double* u, double* uacc) {
-  __shared__ GateSlot slot;
-  const int lane = threadIdx.x;
-  Xoshiro st = stream_init(seed, p);
-  if (initial == 1) {
-    const uint64_t draws = uint64_t{2} << spins;
-    for (uint64_t i = 0; i < draws; ++i) next_u64(st);
-  }
-  for (uint64_t s = 0; s < steps; ++s) {
-    produce_gate(st, lane, spins, &slot, 0.0);
-    __syncwarp();
-    if (lane < 16) {
-      // back to column-major interleaved U(x,y) at 2*(x + 4y)
-      const int x = lane >> 2, y = lane & 3;
-      u[s * 32 + 2 * (x + 4 * y)] = slot.ur[lane];
-      u[s * 32 + 2 * (x + 4 * y) + 1] = slot.ui[lane];
+__global__ void probe_unpack_kernel(const GateRec* recs, uint64_t steps, uint8_t* sites, double* u,
+                                    double* uacc) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= steps) return;
+  const GateRec& g = recs[i];
+  for (int x = 0; x < 4; ++x)
+    for (int y = 0; y < 4; ++y) {  // back to column-major interleaved U(x,y) at 2*(x + 4y)
+      u[i * 32 + 2 * (x + 4 * y)] = g.ur[x * 4 + y];
+      u[i * 32 + 2 * (x + 4 * y) + 1] = g.ui[x * 4 + y];
     }
-    if (lane == 0) {
-      sites[s] = static_cast<uint8_t>(slot.site);
-      uacc[s] = slot.uacc;
-    }
-    __syncwarp();
-  }
+  sites[i] = static_cast<uint8_t>(g.site);
+  uacc[i] = g.u;
 }
 
 // Loads interleaved complex psi (2^S) into the planar padded SMEM layout.
@@ -57,7 +43,7 @@ template <int LA, int LB>
 __global__ void apply_gate_smem_kernel(const double* psi, int site, const double* u, double* out) {
   using D = smem::Dims<LA, LB>;
   extern __shared__ __align__(128) unsigned char raw[];
-  GateSlot& g = *reinterpret_cast<GateSlot*>(raw);
+  GateRec& g = *reinterpret_cast<GateRec*>(raw);
   double* planes = reinterpret_cast<double*>(raw + 512);
   const int tid = threadIdx.x;
   if (tid < 16) {
@@ -66,7 +52,7 @@ __global__ void apply_gate_smem_kernel(const double* psi, int site, const double
     g.ui[tid] = u[2 * (x + 4 * y) + 1];
   }
   load_state<D>(psi, planes, planes + D::PLANE, tid, blockDim.x);
-  smem::gate_pass<D>(planes, planes + D::PLANE, planes + 2 * D::PLANE, planes + 3 * D::PLANE,
+  smem::gate_pass_fma<D>(planes, planes + D::PLANE, planes + 2 * D::PLANE, planes + 3 * D::PLANE,
                      site, g, tid, blockDim.x);
   __syncthreads();
   for (int idx = tid; idx < D::N; idx += blockDim.x) {
@@ -150,10 +136,31 @@ cudaError_t probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* d_out, cu
   return cudaGetLastError();
 }
 
+// The production pre-pass (gate_stream.cu) for one replica; records copied out.
 cudaError_t probe_gates(uint32_t spins, uint64_t seed, uint64_t p, uint64_t steps, int initial,
                         uint8_t* d_sites, double* d_u, double* d_uacc, cudaStream_t s) {
-  gates_kernel<<<1, 32, 0, s>>>(spins, seed, p, steps, initial, d_sites, d_u, d_uacc);
-  return cudaGetLastError();
+  AnnealParams ap{};
+  ap.spins = spins;
+  ap.initial_state = initial;
+  ap.steps = steps;
+  ap.seed = seed;
+  ap.t0 = 1.0;
+  ap.t_min = 1e-3;
+  ap.rows = 1;
+  ap.p_first = p;
+  ap.p_stride = 1;
+  const size_t bytes = gate_stream_bytes_per_row(spins, steps, initial);
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, bytes, s);
+  if (e != cudaSuccess) return e;
+  GateStream gs{};
+  e = launch_gate_stream(ap, ws, bytes, &gs, s);
+  if (e == cudaSuccess && steps > 0) {
+    probe_unpack_kernel<<<static_cast<unsigned>((steps + 127) / 128), 128, 0, s>>>(gs.recs, steps, d_sites, d_u, d_uacc);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(ws, s);
+  return e;
 }
 
 cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const double* u,

@@ -20,8 +20,6 @@ namespace smem {
 
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kThreads = kConsumers + 32;  // + 1 producer warp
-constexpr int kRing = 8;                   // gate slots in flight
 
 template <int LA, int LB>
 struct Dims {
@@ -38,7 +36,7 @@ struct Dims {
   }
 };
 
-// Warp tiling of the NB x NB block grid over the 8 consumer warps.
+// Warp tiling of the NB x NB block grid over the 8 GEMM warps.
 template <int NB>
 struct Tile {
   static constexpr int TM = NB >= 8 ? 2 : 1;
@@ -47,10 +45,7 @@ struct Tile {
   static_assert(WR * WC <= kConsumerWarps, "tiling");
 };
 
-struct Header {
-  GateSlot ring[kRing];
-  uint64_t full[kRing];
-  uint64_t empty[kRing];
+struct Header {  // HBM tier CTA scratch
   double part_rho[kConsumerWarps];
   double part_tr[kConsumerWarps];
   int32_t decision;
@@ -58,18 +53,17 @@ struct Header {
 };
 constexpr int kHeaderBytes = (static_cast<int>(sizeof(Header)) + 127) / 128 * 128;
 
-template <int LA, int LB>
-constexpr int smem_bytes() {
-  return kHeaderBytes + 4 * Dims<LA, LB>::PLANE * 8;
-}
-
-// Gate application (spinmc.cpp:91-136) planar SMEM -> planar SMEM, reference rounding:
-// re += ur*vr - ui*vi; im += ur*vi + ui*vr, ascending y, no FMA contraction.
-template <class D>
-__device__ __forceinline__ void gate_pass(const double* __restrict__ sx,
-                                          const double* __restrict__ sy, double* __restrict__ dx,
-                                          double* __restrict__ dy, int site,
-                                          const GateSlot& g, int tid, int nthreads) {
+// Gate application (spinmc.cpp:91-136) planar SMEM -> planar SMEM, fused form:
+// re = fma(-ui, vi, fma(ur, vr, re)); im = fma(ui, vr, fma(ur, vi, im)), ascending y.
+// Same sum as the reference (re += ur*vr - ui*vi) with fused rounding: 64 DFMA per group
+// instead of 128 DMUL/DADD. On sm_100a DMMA and DFMA share the FP64 pipe, so the gate's
+// op count is paid directly out of the GEMM's budget; the result differs from the
+// reference's unfused rounding by ~1 ulp (parity is within tolerance).
+template <class D, class R>  // R: anything with ur[16], ui[16] (GateRec)
+__device__ __forceinline__ void gate_pass_fma(const double* __restrict__ sx,
+                                              const double* __restrict__ sy,
+                                              double* __restrict__ dx, double* __restrict__ dy,
+                                              int site, const R& g, int tid, int nthreads) {
   double ur[16], ui[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
@@ -78,6 +72,7 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx,
   }
   constexpr int GROUPS = D::N / 4;
   const int lo_mask = (1 << site) - 1;
+#pragma unroll 2
   for (int gi = tid; gi < GROUPS; gi += nthreads) {
     const int base = ((gi >> site) << (site + 2)) | (gi & lo_mask);
     int ph[4];
@@ -93,8 +88,8 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx,
       double re = 0.0, im = 0.0;
 #pragma unroll
       for (int y = 0; y < 4; ++y) {
-        re = __dadd_rn(re, __dsub_rn(__dmul_rn(ur[x * 4 + y], vr[y]), __dmul_rn(ui[x * 4 + y], vi[y])));
-        im = __dadd_rn(im, __dadd_rn(__dmul_rn(ur[x * 4 + y], vi[y]), __dmul_rn(ui[x * 4 + y], vr[y])));
+        re = fma(-ui[x * 4 + y], vi[y], fma(ur[x * 4 + y], vr[y], re));
+        im = fma(ui[x * 4 + y], vr[y], fma(ur[x * 4 + y], vi[y], im));
       }
       dx[ph[x]] = re;
       dy[ph[x]] = im;

@@ -2,10 +2,8 @@
 //
 //  * xoshiro256++ / splitmix64 seeding: bit-exact port of rng.cpp:12-59 (integer work).
 //  * Box-Muller (rng.cpp:61-67) with CUDA libm log/sqrt/sincos (<= 2 ulp vs glibc).
-//  * Haar 4x4 unitary (spinmc.cpp:65-89): Ginibre fill + modified Gram-Schmidt, run by
-//    the producer warp, 4 lanes = 4 rows, unfused rounding (__dmul_rn/__dadd_rn) so that
-//    for identical G the result is bitwise the reference's.
-//  * mbarrier ring protocol between the producer warp and the consumer warps.
+//  * GateRec: one pre-generated proposal (gate_stream.cu builds the stream).
+//  * mbarrier / cp.async helpers.
 //  * FP64 tensor op: mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4 (the only FP64 MMA shape on
 //    sm_100a; there is no tcgen05 kind for f64).
 #pragma once
@@ -85,87 +83,20 @@ __device__ __forceinline__ void box_muller(uint64_t x1, uint64_t x2, double& a, 
   b = __dmul_rn(r, s);
 }
 
-// ------------------------------------------------------------------- gate ring slot
-// One Metropolis proposal, data-independent of the trajectory: the
-// producer warp writes it steps ahead of the consumers.
-struct GateSlot {
-  double ur[16];   // U(x,y).re at x*4+y  (row-major: x = output basis index)
+// -------------------------------------------------------------- gate stream record
+// One proposal of one replica, produced by the pre-pass (gate_stream.cu). 288 bytes.
+struct GateRec {
+  double ur[16];  // U(x,y).re at x*4+y (row-major: x = output basis index)
   double ui[16];
-  double uacc;     // uniform01 acceptance draw (spinmc.cpp:207)
-  double temp;     // temperature(step)           (spinmc.cpp:178-184)
-  int32_t site;    // uniform_index(S-1)          (spinmc.cpp:198)
+  double u;       // uniform01 acceptance draw (spinmc.cpp:207)
+  double temp;    // temperature(step) (spinmc.cpp:178-184)
+  double emul;    // decision factor: exp(-T log u) (maximize) / exp(T log u) (minimize)
+  int32_t site;   // uniform_index(S-1) (spinmc.cpp:198)
   int32_t pad;
 };
+static_assert(sizeof(GateRec) == 288, "GateRec layout");
 
-// Producer: generate the gate of one step. All 32 lanes hold the SAME xoshiro state and
-// advance it identically (34 draws), so control flow is warp-uniform. Lanes 0..15 each
-// produce one normal pair (element (k&3, k>>2) of G, column-major fill spinmc.cpp:68-73);
-// lanes 0..3 then run MGS as the 4 rows. Writes the slot (lanes 0..3) — caller fences.
-__device__ __forceinline__ void produce_gate(Xoshiro& st, int lane, uint32_t spins,
-                                             GateSlot* slot, double temp) {
-  const uint32_t site = uniform_index(st, static_cast<uint64_t>(spins - 1));
-  uint64_t d1 = 0, d2 = 0;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const uint64_t x = next_u64(st);
-    if (j == 2 * lane) d1 = x;
-    if (j == 2 * lane + 1) d2 = x;
-  }
-  const uint64_t dacc = next_u64(st);
-  double gr = 0.0, gi = 0.0;
-  if (lane < 16) box_muller(d1, d2, gr, gi);
-  // lane i (0..3) gathers row i: q(i,j) lives on lane i + 4j.
-  const int row = lane & 3;
-  double qr[4], qi[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    qr[j] = __shfl_sync(0xffffffffu, gr, row + 4 * j);
-    qi[j] = __shfl_sync(0xffffffffu, gi, row + 4 * j);
-  }
-  // Modified Gram-Schmidt, spinmc.cpp:77-87, reductions over i in ascending order.
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int prev = 0; prev < j; ++prev) {
-      // term_i = conj(q(i,prev)) * q(i,j) = (ar*br - ai*bi, ar*bi + ai*br), ai = -q.im
-      const double ar = qr[prev], ai = -qi[prev];
-      const double tr = __dsub_rn(__dmul_rn(ar, qr[j]), __dmul_rn(ai, qi[j]));
-      const double ti = __dadd_rn(__dmul_rn(ar, qi[j]), __dmul_rn(ai, qr[j]));
-      double pr = 0.0, pi = 0.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        pr = __dadd_rn(pr, __shfl_sync(0xffffffffu, tr, i));
-        pi = __dadd_rn(pi, __shfl_sync(0xffffffffu, ti, i));
-      }
-      // q(i,j) -= proj * q(i,prev)
-      const double sr = __dsub_rn(__dmul_rn(pr, qr[prev]), __dmul_rn(pi, qi[prev]));
-      const double si = __dadd_rn(__dmul_rn(pr, qi[prev]), __dmul_rn(pi, qr[prev]));
-      qr[j] = __dsub_rn(qr[j], sr);
-      qi[j] = __dsub_rn(qi[j], si);
-    }
-    const double t = __dadd_rn(__dmul_rn(qr[j], qr[j]), __dmul_rn(qi[j], qi[j]));
-    double nrm = 0.0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) nrm = __dadd_rn(nrm, __shfl_sync(0xffffffffu, t, i));
-    nrm = __dsqrt_rn(nrm);
-    qr[j] = __ddiv_rn(qr[j], nrm);
-    qi[j] = __ddiv_rn(qi[j], nrm);
-  }
-  if (lane < 4) {
-#pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      slot->ur[lane * 4 + y] = qr[y];
-      slot->ui[lane * 4 + y] = qi[y];
-    }
-  }
-  if (lane == 0) {
-    slot->site = static_cast<int32_t>(site);
-    slot->uacc = u01(dacc);
-    slot->temp = temp;
-  }
-}
-
-// spinmc.cpp:178-184 (producer-side: the schedule is data-independent)
+// spinmc.cpp:178-184 (the schedule is data-independent: computed by the pre-pass)
 __device__ __forceinline__ double temperature(double t0, double t_min, uint64_t step,
                                               uint64_t total) {
   const double frac = __ddiv_rn(static_cast<double>(step), static_cast<double>(total));
@@ -214,6 +145,15 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

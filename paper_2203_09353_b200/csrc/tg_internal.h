@@ -7,6 +7,8 @@
 
 namespace tg {
 
+struct GateRec;  // tg_device.cuh
+
 // Everything one persistent anneal launch needs. Rows r in [0, rows) are replicas
 // p = p_first + r * p_stride (p mod devices / shard binding, bench.cpp:171).
 struct AnnealParams {
@@ -25,8 +27,19 @@ struct AnnealParams {
   double* final_entropy;
   int32_t* status;
   int64_t* status_step;
-  double* workspace;  // HBM tier: per-CTA psi/psi' slabs
+  double* workspace;  // HBM tier: per-CTA psi/psi' slabs; TRACE probe: phase stamps
+  const GateRec* gates;        // [rows][steps] proposal stream (gate_stream.cu)
+  const double* init_states;   // [rows][2^S] interleaved, unnormalised (random start) or null
 };
+
+// Pre-generated proposal stream of one launch (gate_stream.cu).
+struct GateStream {
+  GateRec* recs;
+  double* init_states;
+};
+size_t gate_stream_bytes_per_row(uint32_t spins, uint64_t steps, int random_init);
+cudaError_t launch_gate_stream(const AnnealParams& p, void* ws, size_t ws_bytes, GateStream* gs,
+                               cudaStream_t stream);
 
 // Status codes written per row by the kernels.
 enum : int32_t { kRowOk = 0, kRowNotNormalized = 2 };
@@ -34,7 +47,8 @@ enum : int32_t { kRowOk = 0, kRowNotNormalized = 2 };
 constexpr int kSmemMaxSpins = 12;
 
 // anneal_smem.cu (S <= 12)
-cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* grid_out);
+cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* grid_out,
+                               bool trace = false);
 // anneal_hbm.cu (S >= 13)
 cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out);
 size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device);

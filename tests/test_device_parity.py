@@ -50,12 +50,21 @@ def test_t2_t3_gate_stream(oracle, spins, initial):
 
 
 # ------------------------------------------------------------------- T4 gate application
-def test_t4_gate_bitwise(kats):
+# S <= 12 applies the gate in fused (DFMA) form — DMMA and DFMA share the FP64 pipe on
+# sm_100a, so halving the gate's op count is worth ~6% of the step: within
+# a few ulp of the reference's unfused rounding. S >= 13 keeps the unfused form: bitwise.
+GATE_TOL = 4 * np.finfo(np.float64).eps
+
+
+def test_t4_gate_vs_reference(kats):
     for i in range(int(kats["n_gates"])):
         spins, site = (int(x) for x in kats[f"gate{i}_meta"])
         got = tg.probe_apply_gate(spins, kats[f"gate{i}_in"], site, kats[f"gate{i}_u"])
         want = kats[f"gate{i}_out"]
-        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (spins, site)
+        if spins <= 12:
+            assert np.abs(got - want).max() <= GATE_TOL * np.abs(want).max(), (spins, site)
+        else:
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (spins, site)
 
 
 @pytest.mark.parametrize("spins", [14, 16])

@@ -1,0 +1,30 @@
+"""Per-phase cycle breakdown of the SMEM-tier anneal kernel (CTA 0, first replica).
+
+    python tools/phase_trace.py [spins] [replicas] [steps]
+
+Stamps (clock64): 0 step start, 1 gate pass done, 2 GEMM done (partials posted),
+3 decision done.
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2203_09353_b200 as tg  # noqa: E402
+
+spins = int(sys.argv[1]) if len(sys.argv) > 1 else 12
+replicas = int(sys.argv[2]) if len(sys.argv) > 2 else 148
+steps = int(sys.argv[3]) if len(sys.argv) > 3 else 200
+t = tg.probe_phase_trace(spins, replicas, steps).astype(np.float64)
+s, nxt = t[10:-2], t[11:-1]
+rows = {
+    "step": nxt[:, 0] - s[:, 0],
+    "gate pass (+ barrier)": s[:, 1] - s[:, 0],
+    "GEMM (+ partials barrier)": s[:, 2] - s[:, 1],
+    "decision (thread 0)": s[:, 3] - s[:, 2],
+    "decision -> next step start": nxt[:, 0] - s[:, 3],
+}
+print(f"S={spins} replicas={replicas} steps={steps}")
+for k, v in rows.items():
+    print(f"  {k:32s} median {np.median(v):8.0f} clk   mean {np.mean(v):8.0f}")
