@@ -144,6 +144,12 @@ tg_status tg_zgemm_strided_launch(int batch, int m, int n, int k, const double a
                                   int64_t strideC, double* out, int64_t strideOut,
                                   int inject_fault, void* stream);
 
+/* Process-global fault hook = linalg::testhooks::perturb_gemm (linalg.hpp:74-79): while set,
+ * every device GEMM (anneal kernels, batched ZGEMM, entropy probe) flips the sign of the
+ * first accumulation term of element (0,0). Exists so verification suites can prove they
+ * catch a broken kernel; never set outside tests. */
+tg_status tg_set_perturb_gemm(int on);
+
 /* FP64 DMMA.8x8x4 throughput probe (all SMs, register-resident): the roofline
  * denominator (no FP64 entry exists in MEASURED_PEAKS.json). */
 tg_status tg_fp64_dmma_peak(int device, double* tflops, double* sm_clock_ghz_est);

@@ -100,7 +100,7 @@ EXPORTS = [
     "tg_anneal_rows", "tg_step_flops", "tg_anneal_run", "tg_anneal_launch",
     "tg_anneal_workspace_bytes", "tg_zgemm_batched", "tg_zgemm_strided_launch",
     "tg_fp64_dmma_peak", "tg_probe_rng", "tg_probe_gates", "tg_probe_apply_gate",
-    "tg_probe_entropy", "tg_probe_phase_trace",
+    "tg_probe_entropy", "tg_probe_phase_trace", "tg_set_perturb_gemm",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -142,6 +142,7 @@ def lib() -> C.CDLL:
     L.tg_probe_gates.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _u8p, _dp, _dp]
     L.tg_probe_apply_gate.argtypes = [C.c_uint32, _dp, C.c_int, _dp, _dp]
     L.tg_probe_entropy.argtypes = [C.c_uint32, C.c_uint64, _dp, _dp, _dp]
+    L.tg_set_perturb_gemm.argtypes = [C.c_int]
     L.tg_probe_phase_trace.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64)]
     for name in EXPORTS:
         if name not in ("tg_last_error", "tg_version", "tg_anneal_rows", "tg_step_flops",

@@ -170,7 +170,7 @@ __global__ void gate_probe_kernel(int spins, const double* psi, int site, const 
 
 __global__ void __launch_bounds__(kConsumers, 1) entropy_probe_kernel(int spins, const double* psi_all,
                                                                        double* scratch, double* e_out,
-                                                                       double* n_out) {
+                                                                       double* n_out, bool fault) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double part[2][kConsumerWarps];
   double* stages = reinterpret_cast<double*>(smem_raw);
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kConsumers, 1) entropy_probe_kernel(int spins,
   __threadfence_block();
   __syncthreads();
   double rho2, tr;
-  rho_partials(G, X, Y, stages, tid, warp, lane, false, rho2, tr);
+  rho_partials(G, X, Y, stages, tid, warp, lane, fault, rho2, tr);
   if (lane == 0) {
     part[0][warp] = rho2;
     part[1][warp] = tr;
@@ -216,7 +216,7 @@ cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const 
 }
 
 cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* e_out,
-                          double* n_out, cudaStream_t s) {
+                          double* n_out, bool fault, cudaStream_t s) {
   if (spins < 13 || spins > 24) return cudaErrorInvalidValue;
   double* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, sizeof(double) * 2 * (size_t{1} << spins) * count, s);
@@ -224,7 +224,7 @@ cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, dou
   const int bytes = kStages * kStage * 8;
   cudaFuncSetAttribute(entropy_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   entropy_probe_kernel<<<static_cast<unsigned>(count), kConsumers, bytes, s>>>(
-      static_cast<int>(spins), psi, scratch, e_out, n_out);
+      static_cast<int>(spins), psi, scratch, e_out, n_out, fault);
   e = cudaGetLastError();
   cudaFreeAsync(scratch, s);
   return e;

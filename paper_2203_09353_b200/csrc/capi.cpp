@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -24,6 +25,7 @@
 namespace {
 
 thread_local std::string g_err;
+std::atomic<int> g_perturb{0};  // tg_set_perturb_gemm
 
 tg_status fail(tg_status s, const std::string& msg) {
   g_err = msg;
@@ -98,7 +100,7 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
   p.spins = c->spins;
   p.objective = c->objective;
   p.initial_state = c->initial_state;
-  p.inject_fault = c->inject_fault;
+  p.inject_fault = c->inject_fault || g_perturb.load();
   p.steps = c->steps;
   p.seed = c->seed;
   p.renorm = c->renormalize_interval;
@@ -422,7 +424,7 @@ tg_status tg_zgemm_strided_launch(int batch, int m, int n, int k, const double a
   if (m < 1 || n < 1 || k < 1) return fail(TG_EINVAL, "gemm: dims must be >= 1");
   if (!alpha || !beta || !A || !B || !out) return fail(TG_EINVAL, "gemm: NULL operand");
   cudaError_t e = tg::launch_zgemm_strided(batch, m, n, k, alpha[0], alpha[1], A, sA, B, sB, beta[0],
-                                           beta[1], C, sC, out, sO, inject_fault,
+                                           beta[1], C, sC, out, sO, inject_fault || g_perturb.load(),
                                            static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "zgemm launch");
   return TG_OK;
@@ -457,7 +459,8 @@ tg_status tg_zgemm_batched(tg_ctx* ctx, int device, int batch, int m, int n, int
   }
   TG_CUDA(cudaEventRecord(d.ev0, d.stream));
   cudaError_t e = tg::launch_zgemm_strided(batch, m, n, k, alpha[0], alpha[1], dA, ea / 2, dB, eb / 2,
-                                           beta[0], beta[1], dC, ec / 2, dO, ec / 2, 0, d.stream);
+                                           beta[0], beta[1], dC, ec / 2, dO, ec / 2, g_perturb.load(),
+                                           d.stream);
   if (e != cudaSuccess) return cuda_fail(e, "zgemm launch");
   TG_CUDA(cudaEventRecord(d.ev1, d.stream));
   for (int i = 0; i < batch; ++i)
@@ -482,6 +485,11 @@ tg_status tg_zgemm_batched(tg_ctx* ctx, int device, int batch, int m, int n, int
       records[i].flops = 8ull * m * n * k;
     }
   }
+  return TG_OK;
+}
+
+tg_status tg_set_perturb_gemm(int on) {
+  g_perturb.store(on ? 1 : 0);
   return TG_OK;
 }
 
@@ -549,7 +557,7 @@ tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, do
   TG_CUDA(cudaMalloc(&d, 8 * (2 * n * count + 2 * count)));
   double *dp = d, *de = d + 2 * n * count, *dn = de + count;
   cudaError_t e = cudaMemcpy(dp, psi, 16 * n * count, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = tg::probe_entropy(spins, count, dp, de, dn, nullptr);
+  if (e == cudaSuccess) e = tg::probe_entropy(spins, count, dp, de, dn, g_perturb.load() != 0, nullptr);
   if (e == cudaSuccess) e = cudaMemcpy(entropy, de, 8 * count, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess && norms) e = cudaMemcpy(norms, dn, 8 * count, cudaMemcpyDeviceToHost);
   cudaFree(d);

@@ -185,7 +185,7 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
 cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const double* u,
                              double* out, cudaStream_t s);
 cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* e,
-                          double* n, cudaStream_t s);
+                          double* n, bool fault, cudaStream_t s);
 
 }  // namespace hbm
 }  // namespace tg

@@ -62,7 +62,7 @@ __global__ void apply_gate_smem_kernel(const double* psi, int site, const double
 }
 
 template <int LA, int LB>
-__global__ void entropy_smem_kernel(const double* psi_all, double* e_out, double* n_out) {
+__global__ void entropy_smem_kernel(const double* psi_all, double* e_out, double* n_out, bool fault) {
   using D = smem::Dims<LA, LB>;
   extern __shared__ __align__(128) unsigned char raw[];
   __shared__ double part[2][smem::kConsumerWarps];
@@ -71,7 +71,7 @@ __global__ void entropy_smem_kernel(const double* psi_all, double* e_out, double
   const double* psi = psi_all + 2ull * D::N * blockIdx.x;
   load_state<D>(psi, planes, planes + D::PLANE, tid, blockDim.x);
   double rho2, tr;
-  smem::rho_partials<D>(planes, planes + D::PLANE, warp, lane, false, rho2, tr);
+  smem::rho_partials<D>(planes, planes + D::PLANE, warp, lane, fault, rho2, tr);
   if (lane == 0) {
     part[0][warp] = rho2;
     part[1][warp] = tr;
@@ -100,13 +100,14 @@ cudaError_t gate_s(const double* psi, int site, const double* u, double* out, cu
 }
 
 template <int S>
-cudaError_t entropy_s(uint64_t count, const double* psi, double* e, double* n, cudaStream_t s) {
+cudaError_t entropy_s(uint64_t count, const double* psi, double* e, double* n, bool fault,
+                      cudaStream_t s) {
   constexpr int LA = S / 2, LB = S - S / 2;
   using D = smem::Dims<LA, LB>;
   const int bytes = 2 * D::PLANE * 8;
   auto k = entropy_smem_kernel<LA, LB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  k<<<static_cast<unsigned>(count), smem::kConsumers, bytes, s>>>(psi, e, n);
+  k<<<static_cast<unsigned>(count), smem::kConsumers, bytes, s>>>(psi, e, n, fault);
   return cudaGetLastError();
 }
 
@@ -182,20 +183,20 @@ cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const 
 }
 
 cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* e,
-                          double* n, cudaStream_t s) {
+                          double* n, bool fault, cudaStream_t s) {
   switch (spins) {
-    case 2: return entropy_s<2>(count, psi, e, n, s);
-    case 3: return entropy_s<3>(count, psi, e, n, s);
-    case 4: return entropy_s<4>(count, psi, e, n, s);
-    case 5: return entropy_s<5>(count, psi, e, n, s);
-    case 6: return entropy_s<6>(count, psi, e, n, s);
-    case 7: return entropy_s<7>(count, psi, e, n, s);
-    case 8: return entropy_s<8>(count, psi, e, n, s);
-    case 9: return entropy_s<9>(count, psi, e, n, s);
-    case 10: return entropy_s<10>(count, psi, e, n, s);
-    case 11: return entropy_s<11>(count, psi, e, n, s);
-    case 12: return entropy_s<12>(count, psi, e, n, s);
-    default: return hbm::probe_entropy(spins, count, psi, e, n, s);
+    case 2: return entropy_s<2>(count, psi, e, n, fault, s);
+    case 3: return entropy_s<3>(count, psi, e, n, fault, s);
+    case 4: return entropy_s<4>(count, psi, e, n, fault, s);
+    case 5: return entropy_s<5>(count, psi, e, n, fault, s);
+    case 6: return entropy_s<6>(count, psi, e, n, fault, s);
+    case 7: return entropy_s<7>(count, psi, e, n, fault, s);
+    case 8: return entropy_s<8>(count, psi, e, n, fault, s);
+    case 9: return entropy_s<9>(count, psi, e, n, fault, s);
+    case 10: return entropy_s<10>(count, psi, e, n, fault, s);
+    case 11: return entropy_s<11>(count, psi, e, n, fault, s);
+    case 12: return entropy_s<12>(count, psi, e, n, fault, s);
+    default: return hbm::probe_entropy(spins, count, psi, e, n, fault, s);
   }
 }
 

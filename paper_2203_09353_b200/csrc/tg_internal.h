@@ -60,7 +60,7 @@ cudaError_t probe_gates(uint32_t spins, uint64_t seed, uint64_t p, uint64_t step
 cudaError_t probe_apply_gate(uint32_t spins, const double* d_psi, int site, const double* d_u,
                              double* d_out, cudaStream_t s);
 cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* d_psi, double* d_e,
-                          double* d_norm, cudaStream_t s);
+                          double* d_norm, bool fault, cudaStream_t s);
 cudaError_t fp64_dmma_peak(double* tflops, double* clock_ghz);
 
 // zgemm.cu
