@@ -168,10 +168,9 @@ tg_status tg_probe_apply_gate(uint32_t spins, const double* psi, int site, const
 tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* entropy,
                            double* norms);
 
-/* Profiling probe: runs `replicas` replicas (S <= 12) and returns clock64 phase stamps of
- * CTA 0's first replica, trace[steps][8]: 0 GEMM start, 1 GEMM end, 2 partials reduced,
- * 3 decision written, 4/5 speculative gate start/end, 6 decision seen by gate warps,
- * 7 proposal published. */
+/* Profiling probe: runs `replicas` replicas and returns clock64 phase stamps of CTA 0's
+ * first replica, trace[steps][8]: 0 step start, 1 gate pass done, 2 GEMM done,
+ * 3 decision done. */
 tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* trace);
 
 #ifdef __cplusplus

@@ -1,144 +1,228 @@
 // anneal_hbm.cu — persistent annealing kernel, HBM/L2-resident tier (13 <= S <= 24).
-// Same warp roles and step protocol as anneal_smem.cu; psi/psi' live in this CTA's
-// workspace slab, rho tiles are staged through SMEM (hbm_tier.cuh).
+//
+// A cluster of CS CTAs (1 or 2, see hbm_tier.cuh) owns one replica at a time; its psi /
+// psi' slabs live in the workspace. Per step (metropolis_step, spinmc.cpp:193-213):
+//   gate pass  — rank k applies U to its half of the groups (reference rounding), global
+//                -> global; cluster barrier;
+//   GEMM       — rho tiles of the rank's parity on DMMA, fused ||rho||_F^2 and trace;
+//                per-rank chain values exchanged through DSMEM; cluster barrier;
+//   decision   — thread 0 of every rank evaluates the same reference formula on the same
+//                totals (identical results); rank 0 writes the trace.
+// Every FP64 op outside the GEMM runs while no DMMA is in flight on the SM (the FP64 pipe
+// is shared, profiles/r01_fp64_contention.txt). The proposal stream comes from the
+// pre-pass (gate_stream.cu).
+#include <cstdlib>
+
 #include "hbm_tier.cuh"
 #include "tg_internal.h"
 
 namespace tg {
 namespace hbm {
 
-__device__ void renormalize(const Geo& G, double* X, double* Y, int tid, int warp, int lane,
-                            Header& H) {
-  double s = 0.0;
-  for (int i = tid; i < G.n; i += kConsumers) {
-    const double x = __ldcg(X + i), y = __ldcg(Y + i);
-    s = fma(x, x, s);
-    s = fma(y, y, s);
+struct HHeader {
+  double part[kWarps][4];  // per-warp chain values {rho even, rho odd, tr even, tr odd}
+  double val[2][4];        // per-rank totals (rank 1's arrive by DSMEM)
+  double norm_half[2];
+  int32_t decision;
+  int32_t error;
+};
+constexpr int kHHeaderBytes = (static_cast<int>(sizeof(HHeader)) + 127) / 128 * 128;
+constexpr int kSmemBytes = kHHeaderBytes + kStages * kStage * 8;
+
+template <int CS>
+__device__ __forceinline__ void sync_all() {
+  if constexpr (CS == 1) {
+    __syncthreads();
+  } else {
+    cluster_sync();
   }
-  s = warp_sum(s);
-  if (lane == 0) H.part_tr[warp] = s;
-  consumer_sync(kConsumers);
-  double tot = 0.0;
+}
+
+// Per-rank values (sum of the per-warp chain values in warp order) published to every rank.
+template <int CS>
+__device__ __forceinline__ void publish_vals(HHeader& H, int tid, uint32_t rank) {
+  __syncthreads();  // per-warp parts written
+  if (tid == 0) {
+    double v[4];
 #pragma unroll
-  for (int w = 0; w < kConsumerWarps; ++w) tot += H.part_tr[w];
-  const double inv = __ddiv_rn(1.0, __dsqrt_rn(tot));
-  for (int i = tid; i < G.n; i += kConsumers) {
+    for (int c = 0; c < 4; ++c) {
+      v[c] = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) v[c] += H.part[w][c];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if constexpr (CS == 1) {
+        H.val[0][c] = v[c];
+      } else {
+        H.val[rank][c] = v[c];
+        st_cluster_f64(&H.val[rank][c], rank ^ 1u, v[c]);
+      }
+    }
+  }
+  sync_all<CS>();
+}
+
+// Totals in the canonical order: even-tile chain + odd-tile chain.
+template <int CS>
+__device__ __forceinline__ void totals(const HHeader& H, double& rho2, double& tr) {
+  if constexpr (CS == 1) {
+    rho2 = H.val[0][0] + H.val[0][1];
+    tr = H.val[0][2] + H.val[0][3];
+  } else {
+    rho2 = H.val[0][0] + H.val[1][1];
+    tr = H.val[0][2] + H.val[1][3];
+  }
+}
+
+// renormalize (spinmc.cpp:56-59) over the two halves of psi (rank k owns half k); the
+// total is half0 + half1 whatever CS is, so CS=1 and CS=2 agree bitwise.
+template <int CS>
+__device__ void renormalize(const Geo& G, double* X, double* Y, int tid, int warp, int lane,
+                            uint32_t rank, HHeader& H) {
+  const int half = G.n / 2;
+  for (int h = 0; h < 2; ++h) {
+    if (CS == 2 && h != static_cast<int>(rank)) continue;
+    double s = 0.0;
+    for (int i = h * half + tid; i < (h + 1) * half; i += kThreads) {
+      const double x = __ldcg(X + i), y = __ldcg(Y + i);
+      s = fma(x, x, s);
+      s = fma(y, y, s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) H.part[warp][0] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) t += H.part[w][0];
+      H.norm_half[h] = t;
+      if (CS == 2) st_cluster_f64(&H.norm_half[h], rank ^ 1u, t);
+    }
+    __syncthreads();
+  }
+  sync_all<CS>();
+  const double inv = __ddiv_rn(1.0, __dsqrt_rn(H.norm_half[0] + H.norm_half[1]));
+  const int i0 = CS == 2 ? static_cast<int>(rank) * half : 0, i1 = CS == 2 ? i0 + half : G.n;
+  for (int i = i0 + tid; i < i1; i += kThreads) {
     __stcg(X + i, __dmul_rn(__ldcg(X + i), inv));
     __stcg(Y + i, __dmul_rn(__ldcg(Y + i), inv));
   }
-  __threadfence_block();
-  consumer_sync(kConsumers);
+  __threadfence();
+  sync_all<CS>();
 }
 
+// TRACE: phase stamps (clock64) of the first cluster's first replica into P.trace[steps][8]:
+// 0 step start, 1 gate pass done, 2 GEMM done, 3 decision done (profiling probe only).
+template <bool TRACE, int CS>
 __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Header& H = *reinterpret_cast<Header*>(smem_raw);
-  double* stages = reinterpret_cast<double*>(smem_raw + kHeaderBytes);
+  HHeader& H = *reinterpret_cast<HHeader*>(smem_raw);
+  double* stages = reinterpret_cast<double*>(smem_raw + kHHeaderBytes);
   const Geo G(static_cast<int>(P.spins));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double* slab = P.workspace + static_cast<size_t>(blockIdx.x) * 4 * G.n;
+  const uint32_t rank = CS == 1 ? 0u : cluster_rank();
+  const uint64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+  double* slab = P.workspace + static_cast<size_t>(cid) * 4 * G.n;
   auto PX = [&](int b) { return slab + (2 * b) * static_cast<size_t>(G.n); };
   auto PY = [&](int b) { return slab + (2 * b + 1) * static_cast<size_t>(G.n); };
+  auto mark = [&](uint64_t r, uint64_t s, int k) {
+    if (TRACE && tid == 0 && rank == 0 && r == 0 && s < P.steps) P.trace[s * 8 + k] = clock64();
+  };
+  const int groups = G.n / 4;
+  const int g0 = CS == 2 ? static_cast<int>(rank) * (groups / 2) : 0;
+  const int g1 = CS == 2 ? g0 + groups / 2 : groups;
+  const int first = static_cast<int>(rank), stride = CS;
+  const bool writer = rank == 0;
 
-  for (uint64_t r = blockIdx.x; r < P.rows; r += gridDim.x) {
+  for (uint64_t r = cid; r < P.rows; r += ncl) {
     const GateRec* recs = P.gates + r * P.steps;
-    if (P.initial_state == 0) {
-      for (int i = tid; i < G.n; i += kConsumers) {  // product_state (spinmc.cpp:28-35)
-        __stcg(PX(0) + i, i == 0 ? 1.0 : 0.0);
-        __stcg(PY(0) + i, 0.0);
+    {  // initial state, split by halves of the amplitude index
+      const int i0 = CS == 2 ? static_cast<int>(rank) * (G.n / 2) : 0, i1 = CS == 2 ? i0 + G.n / 2 : G.n;
+      if (P.initial_state == 0) {
+        for (int i = i0 + tid; i < i1; i += kThreads) {  // product_state (spinmc.cpp:28-35)
+          __stcg(PX(0) + i, i == 0 ? 1.0 : 0.0);
+          __stcg(PY(0) + i, 0.0);
+        }
+      } else {  // random_state (spinmc.cpp:37-48), normals from the pre-pass
+        const double* src = P.init_states + r * 2 * static_cast<size_t>(G.n);
+        for (int i = i0 + tid; i < i1; i += kThreads) {
+          __stcg(PX(0) + i, src[2 * i]);
+          __stcg(PY(0) + i, src[2 * i + 1]);
+        }
       }
-    } else {  // random_state (spinmc.cpp:37-48), normals from the pre-pass
-      const double* src = P.init_states + r * 2 * static_cast<size_t>(G.n);
-      for (int i = tid; i < G.n; i += kConsumers) {
-        __stcg(PX(0) + i, src[2 * i]);
-        __stcg(PY(0) + i, src[2 * i + 1]);
-      }
+      __threadfence();
+      sync_all<CS>();
     }
-    __threadfence_block();
-    __syncthreads();
     int cur = 0;
-    if (P.initial_state == 1) renormalize(G, PX(0), PY(0), tid, warp, lane, H);
+    if (P.initial_state == 1) renormalize<CS>(G, PX(0), PY(0), tid, warp, lane, rank, H);
 
-    double rho2, tr;
-    rho_partials(G, PX(cur), PY(cur), stages, tid, warp, lane, P.inject_fault != 0, rho2, tr);
-    if (lane == 0) {
-      H.part_rho[warp] = rho2;
-      H.part_tr[warp] = tr;
-    }
-    consumer_sync(kConsumers);
-    double cur_e = 0.0;
-    if (tid == 0) {
-      double a = 0.0, t = 0.0;
-#pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) {
-        a += H.part_rho[w];
-        t += H.part_tr[w];
-      }
-      H.error = 0;
-      if (smem::not_normalized(t)) {
-        H.error = 1;
-        P.status[r] = kRowNotNormalized;
-        P.status_step[r] = -1;
-      } else {
-        P.status[r] = kRowOk;
-      }
-      cur_e = smem::renyi2(a);
+    double out[4], rho2, tr;
+    rho_partials(G, PX(cur), PY(cur), stages, tid, warp, lane, first, stride, P.inject_fault != 0, out);
+    if (lane == 0)
+      for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
+    publish_vals<CS>(H, tid, rank);
+    totals<CS>(H, rho2, tr);
+    double cur_e = smem::renyi2(rho2);  // spinmc.cpp:234
+    bool err = smem::not_normalized(tr);
+    if (tid == 0 && writer) {
+      P.status[r] = err ? kRowNotNormalized : kRowOk;
+      if (err) P.status_step[r] = -1;
       P.initial_entropy[r] = cur_e;
     }
-    consumer_sync(kConsumers);
-    bool err = H.error != 0;
 
     int64_t t_prev = (tid == 0 && P.wall_ns) ? globaltimer() : 0;
     for (uint64_t s = 0; s < P.steps && !err; ++s) {
       const GateRec& g = recs[s];
-      const int site = g.site;
-      gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), G.spins, site, g, tid, kConsumers);
-      __threadfence_block();
-      consumer_sync(kConsumers);
-      rho_partials(G, PX(cur ^ 1), PY(cur ^ 1), stages, tid, warp, lane, P.inject_fault != 0,
-                   rho2, tr);
-      if (lane == 0) {
-        H.part_rho[warp] = rho2;
-        H.part_tr[warp] = tr;
-      }
-      consumer_sync(kConsumers);
-      if (tid == 0) {
-        double a = 0.0, t = 0.0;
-#pragma unroll
-        for (int w = 0; w < kConsumerWarps; ++w) {
-          a += H.part_rho[w];
-          t += H.part_tr[w];
-        }
+      mark(r, s, 0);
+      gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, kThreads);
+      __threadfence();
+      sync_all<CS>();
+      mark(r, s, 1);
+      rho_partials(G, PX(cur ^ 1), PY(cur ^ 1), stages, tid, warp, lane, first, stride,
+                   P.inject_fault != 0, out);
+      if (lane == 0)
+        for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
+      publish_vals<CS>(H, tid, rank);
+      mark(r, s, 2);
+      totals<CS>(H, rho2, tr);
+      if (tid == 0) {  // every rank decides identically; rank 0 writes
         int acc = 0;
-        if (smem::not_normalized(t)) {
+        if (smem::not_normalized(tr)) {
           H.error = 1;
-          P.status[r] = kRowNotNormalized;
-          P.status_step[r] = static_cast<int64_t>(s);
+          if (writer) {
+            P.status[r] = kRowNotNormalized;
+            P.status_step[r] = static_cast<int64_t>(s);
+          }
         } else {
-          const double proposed = smem::renyi2(a);
+          H.error = 0;
+          const double proposed = smem::renyi2(rho2);
           const double delta = P.objective == 0 ? proposed - cur_e : cur_e - proposed;
           acc = g.u < acceptance(delta, g.temp);
           if (acc) cur_e = proposed;
         }
         H.decision = acc;
-        const uint64_t o = r * P.steps + s;
-        P.entropies[o] = cur_e;
-        P.accepted[o] = static_cast<uint8_t>(acc);
-        if (P.sites) P.sites[o] = static_cast<uint8_t>(site);
-        if (P.wall_ns) {
-          const int64_t t_now = globaltimer();
-          P.wall_ns[o] = t_now - t_prev;
-          t_prev = t_now;
+        if (writer) {
+          const uint64_t o = r * P.steps + s;
+          P.entropies[o] = cur_e;
+          P.accepted[o] = static_cast<uint8_t>(acc);
+          if (P.sites) P.sites[o] = static_cast<uint8_t>(g.site);
+          if (P.wall_ns) {
+            const int64_t t_now = globaltimer();
+            P.wall_ns[o] = t_now - t_prev;
+            t_prev = t_now;
+          }
         }
+        mark(r, s, 3);
       }
-      consumer_sync(kConsumers);
+      __syncthreads();
       err = H.error != 0;
       if (H.decision) cur ^= 1;
       if (!err && P.renorm > 0 && (s + 1) % P.renorm == 0)
-        renormalize(G, PX(cur), PY(cur), tid, warp, lane, H);
+        renormalize<CS>(G, PX(cur), PY(cur), tid, warp, lane, rank, H);  // spinmc.cpp:246-248
     }
-    if (tid == 0 && P.final_entropy) P.final_entropy[r] = cur_e;
-    __syncthreads();  // the slab is rewritten by the next replica
+    if (tid == 0 && writer && P.final_entropy) P.final_entropy[r] = cur_e;
+    sync_all<CS>();  // the slab is rewritten by the cluster's next replica
   }
 }
 
@@ -159,7 +243,7 @@ __global__ void gate_probe_kernel(int spins, const double* psi, int site, const 
   }
   __threadfence_block();
   __syncthreads();
-  gate_pass(scratch, scratch + n, scratch + 2 * n, scratch + 3 * n, spins, site, g, tid, blockDim.x);
+  gate_pass(scratch, scratch + n, scratch + 2 * n, scratch + 3 * n, site, g, 0, n / 4, tid, blockDim.x);
   __threadfence_block();
   __syncthreads();
   for (int i = tid; i < n; i += blockDim.x) {
@@ -168,38 +252,33 @@ __global__ void gate_probe_kernel(int spins, const double* psi, int site, const 
   }
 }
 
-__global__ void __launch_bounds__(kConsumers, 1) entropy_probe_kernel(int spins, const double* psi_all,
-                                                                       double* scratch, double* e_out,
-                                                                       double* n_out, bool fault) {
+__global__ void __launch_bounds__(kThreads, 1) entropy_probe_kernel(int spins, const double* psi_all,
+                                                                     double* scratch, double* e_out,
+                                                                     double* n_out, bool fault) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ double part[2][kConsumerWarps];
-  double* stages = reinterpret_cast<double*>(smem_raw);
+  HHeader& H = *reinterpret_cast<HHeader*>(smem_raw);
+  double* stages = reinterpret_cast<double*>(smem_raw + kHHeaderBytes);
   const Geo G(spins);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const double* psi = psi_all + 2ull * G.n * blockIdx.x;
   double* X = scratch + 2ull * G.n * blockIdx.x;
   double* Y = X + G.n;
-  for (int i = tid; i < G.n; i += kConsumers) {
+  for (int i = tid; i < G.n; i += kThreads) {
     X[i] = psi[2 * i];
     Y[i] = psi[2 * i + 1];
   }
   __threadfence_block();
   __syncthreads();
-  double rho2, tr;
-  rho_partials(G, X, Y, stages, tid, warp, lane, fault, rho2, tr);
-  if (lane == 0) {
-    part[0][warp] = rho2;
-    part[1][warp] = tr;
-  }
-  __syncthreads();
+  double out[4];
+  rho_partials(G, X, Y, stages, tid, warp, lane, 0, 1, fault, out);
+  if (lane == 0)
+    for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
+  publish_vals<1>(H, tid, 0);
   if (tid == 0) {
-    double a = 0.0, t = 0.0;
-    for (int w = 0; w < kConsumerWarps; ++w) {
-      a += part[0][w];
-      t += part[1][w];
-    }
-    e_out[blockIdx.x] = smem::renyi2(a);
-    if (n_out) n_out[blockIdx.x] = __dsqrt_rn(t);
+    double rho2, tr;
+    totals<1>(H, rho2, tr);
+    e_out[blockIdx.x] = smem::renyi2(rho2);
+    if (n_out) n_out[blockIdx.x] = __dsqrt_rn(tr);
   }
 }
 
@@ -209,7 +288,7 @@ cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const 
   double* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, sizeof(double) * 4 * (size_t{1} << spins), s);
   if (e != cudaSuccess) return e;
-  gate_probe_kernel<<<1, kConsumers, 0, s>>>(static_cast<int>(spins), psi, site, u, scratch, out);
+  gate_probe_kernel<<<1, kThreads, 0, s>>>(static_cast<int>(spins), psi, site, u, scratch, out);
   e = cudaGetLastError();
   cudaFreeAsync(scratch, s);
   return e;
@@ -221,13 +300,28 @@ cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, dou
   double* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, sizeof(double) * 2 * (size_t{1} << spins) * count, s);
   if (e != cudaSuccess) return e;
-  const int bytes = kStages * kStage * 8;
-  cudaFuncSetAttribute(entropy_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  entropy_probe_kernel<<<static_cast<unsigned>(count), kConsumers, bytes, s>>>(
+  cudaFuncSetAttribute(entropy_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  entropy_probe_kernel<<<static_cast<unsigned>(count), kThreads, kSmemBytes, s>>>(
       static_cast<int>(spins), psi, scratch, e_out, n_out, fault);
   e = cudaGetLastError();
   cudaFreeAsync(scratch, s);
   return e;
+}
+
+// CTAs per replica: 2 when a partial last wave of SMs would otherwise waste >= 2% of the
+// machine (e.g. 512 replicas on 148 SMs: 86.5% -> 98.8%). TG_HBM_CTAS_PER_REPLICA=1|2
+// overrides (tests use it to check both paths agree bitwise).
+int ctas_per_replica(uint64_t rows, int sms) {
+  if (const char* env = std::getenv("TG_HBM_CTAS_PER_REPLICA")) {
+    const int v = std::atoi(env);
+    if (v == 1 || v == 2) return v;
+  }
+  if (rows == 0) return 1;
+  auto eff = [&](uint64_t units) {
+    const uint64_t waves = (units + sms - 1) / sms;
+    return static_cast<double>(units) / static_cast<double>(waves * sms);
+  };
+  return eff(2 * rows) > eff(rows) + 0.02 ? 2 : 1;
 }
 
 }  // namespace hbm
@@ -235,23 +329,42 @@ cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, dou
 size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  const uint64_t grid = rows < static_cast<uint64_t>(sms) ? rows : static_cast<uint64_t>(sms);
-  return static_cast<size_t>(grid) * 4 * (size_t{1} << spins) * sizeof(double);
+  const int cs = hbm::ctas_per_replica(rows, sms);
+  const uint64_t clusters = std::min<uint64_t>(rows, static_cast<uint64_t>(sms / cs));
+  return static_cast<size_t>(clusters) * 4 * (size_t{1} << spins) * sizeof(double);
 }
 
-cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out) {
+cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out,
+                              bool trace) {
   if (p.spins < 13 || p.spins > 24) return cudaErrorInvalidValue;
   if (!p.workspace) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(hbm::anneal_hbm_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
-  if (e != cudaSuccess) return e;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = static_cast<int>(p.rows < static_cast<uint64_t>(sms) ? p.rows : sms);
+  const int cs = hbm::ctas_per_replica(p.rows, sms);
+  const uint64_t clusters = std::min<uint64_t>(p.rows, static_cast<uint64_t>(sms / cs));
+  const int grid = static_cast<int>(clusters) * cs;
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
-  hbm::anneal_hbm_kernel<<<grid, hbm::kThreads, hbm::kSmemBytes, stream>>>(p);
+  void (*kern)(AnnealParams);
+  if (cs == 1) kern = trace ? hbm::anneal_hbm_kernel<true, 1> : hbm::anneal_hbm_kernel<false, 1>;
+  else kern = trace ? hbm::anneal_hbm_kernel<true, 2> : hbm::anneal_hbm_kernel<false, 2>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(hbm::kThreads);
+  cfg.dynamicSmemBytes = hbm::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -160,9 +160,9 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
     if (e != cudaSuccess) return e;
     q.gates = gs.recs;
     q.init_states = gs.init_states;
-    if (!trace) q.workspace = reinterpret_cast<double*>(slabs);
+    q.workspace = reinterpret_cast<double*>(slabs);
     e = p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::launch_anneal_smem(q, s, nullptr, trace)
-                                                           : tg::launch_anneal_hbm(q, s, nullptr);
+                                                           : tg::launch_anneal_hbm(q, s, nullptr, trace);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -566,8 +566,7 @@ tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, do
 }
 
 tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* trace) {
-  if (spins < 2 || spins > static_cast<uint32_t>(tg::kSmemMaxSpins))
-    return fail(TG_EINVAL, "phase trace covers the SMEM tier (spins <= 12)");
+  if (spins < 2 || spins > 24) return fail(TG_EINVAL, "phase trace covers spins in [2,24]");
   tg_anneal_config c{};
   c.spins = spins;
   c.devices = 1;
@@ -590,7 +589,7 @@ tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps
   p.entropies = carve<double>(cur, replicas * steps);
   p.accepted = carve<uint8_t>(cur, replicas * steps);
   int64_t* tr = carve<int64_t>(cur, 8 * steps);
-  p.workspace = reinterpret_cast<double*>(tr);
+  p.trace = tr;
   int dev = 0;
   cudaGetDevice(&dev);
   const size_t wsb = workspace_for(p, dev);

@@ -1,34 +1,31 @@
-// hbm_tier.cuh — HBM/L2-resident tier (13 <= S <= 24): psi and psi' are per-CTA slabs
-// in the workspace (planar X, Y planes of 2^S doubles, column-major Psi[a][b] at
-// a + b*d_a = amplitude index, spinmc.cpp:145-148). One CTA owns one replica at a time.
+// hbm_tier.cuh — HBM/L2-resident tier (13 <= S <= 24): psi and psi' are slabs in the
+// workspace (planar X, Y planes of 2^S doubles, column-major Psi[a][b] at a + b*d_a =
+// amplitude index, spinmc.cpp:145-148). One replica is owned by a cluster of CS CTAs
+// (CS = 1, or 2 when the replica count would leave a partial last wave of SMs).
 //
-// rho = Psi' Psi'^dagger is computed in 64x64 complex output tiles; for each tile the
-// K = d_b dimension streams through a 2-stage cp.async pipeline of 32-column chunks of
-// the A (rows of tile i) and B (rows of tile j) panels, staged in SMEM with pitch 68
-// doubles (conflict-free DMMA fragments, as in the SMEM tier). Each warp computes a
-// 16x32 sub-tile (2x4 blocks of 8x8) with the real-split DMMA scheme; the epilogue folds
-// sum |rho_ij|^2 and trace(rho) into per-thread running sums — rho is never stored.
+// rho = Psi' Psi'^dagger is computed in 64x64 complex output tiles (row-major tile order
+// t = ti*nt + tj); for each tile K = d_b streams through a 3-stage cp.async pipeline of
+// 32-column chunks of the A (rows of tile i) and B (rows of tile j) panels, staged in
+// SMEM with pitch 68 doubles (conflict-free DMMA fragments). Each warp computes a 16x32
+// sub-tile (2x4 blocks of 8x8) with the real-split DMMA scheme; the epilogue folds
+// sum |rho_ij|^2 and trace(rho) into two running chains, even tiles and odd tiles, and rho
+// is never stored. Rank k of a 2-CTA cluster takes the tiles t = k (mod 2), i.e. exactly
+// one chain, so the result is bitwise the same whether 1 or 2 CTAs share a replica.
 #pragma once
 #include "smem_tier.cuh"
 
 namespace tg {
 namespace hbm {
 
-constexpr int kConsumerWarps = smem::kConsumerWarps;
-constexpr int kConsumers = smem::kConsumers;
-constexpr int kThreads = smem::kConsumers;  // no producer warp: the stream is pre-generated
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
 constexpr int TB = 64;        // output tile (complex rows/cols)
 constexpr int KC = 32;        // K columns per pipeline stage
 constexpr int SP = TB + 4;    // SMEM pitch (doubles)
 constexpr int kPanel = KC * SP;                 // doubles per (panel, plane)
 constexpr int kStage = 4 * kPanel;              // A.X, A.Y, B.X, B.Y
-constexpr int kStages = 2;
+constexpr int kStages = 3;
 using T8 = smem::Tile<8>;                       // TM=2, TN=4, warp grid 4x2
-
-using smem::Header;
-constexpr int kHeaderBytes = smem::kHeaderBytes;
-constexpr int kSmemBytes = kHeaderBytes + kStages * kStage * 8;
-
 
 struct Geo {
   int spins, la, da, db, n;
@@ -37,12 +34,31 @@ struct Geo {
   __device__ int kchunks() const { return db / KC; }
 };
 
-// Gate application (spinmc.cpp:91-136), global planar -> global planar, reference rounding
-// (bitwise the reference's psi' for the same U). R = GateRec (global or SMEM).
+// ------------------------------------------------------------------------- clusters
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// Cluster-wide barrier with release/acquire at cluster scope (orders the global-memory
+// slab writes of one CTA before the other CTA's reads).
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+// Store v at the same SMEM offset as `local` in CTA `rank` of the cluster (DSMEM).
+__device__ __forceinline__ void st_cluster_f64(double* local, uint32_t rank, double v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
+}
+
+// Gate application (spinmc.cpp:91-136) on groups [g0, g1), global planar -> global planar,
+// reference rounding (bitwise the reference's psi' for the same U). R: GateRec.
 template <class R>
 __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const double* __restrict__ sy,
                                           double* __restrict__ dx, double* __restrict__ dy,
-                                          int spins, int site, const R& g, int tid,
+                                          int site, const R& g, int g0, int g1, int tid,
                                           int nthreads) {
   double ur[16], ui[16];
 #pragma unroll
@@ -50,9 +66,8 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const d
     ur[e] = g.ur[e];
     ui[e] = g.ui[e];
   }
-  const int groups = 1 << (spins - 2);
   const int lo_mask = (1 << site) - 1;
-  for (int gi = tid; gi < groups; gi += nthreads) {
+  for (int gi = g0 + tid; gi < g1; gi += nthreads) {
     const int base = ((gi >> site) << (site + 2)) | (gi & lo_mask);
     double vr[4], vi[4];
 #pragma unroll
@@ -74,53 +89,56 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const d
   }
 }
 
-// Issue the cp.async copies of pipeline iteration `it` (tile (ti,tj), chunk kc).
-__device__ __forceinline__ void load_stage(const Geo& G, const double* X, const double* Y, int it,
-                                           double* stage, int tid) {
-  const int nk = G.kchunks(), nt = G.tiles();
-  const int tile = it / nk, kc = it % nk;
-  const int ti = tile / nt, tj = tile % nt;
-  // 4 (panel, plane) pairs x KC columns x 32 row-pairs = 4096 16-byte copies
-#pragma unroll 4
-  for (int c = tid; c < 4 * KC * 32; c += kConsumers) {
-    const int pp = c / (KC * 32);
-    const int rem = c % (KC * 32);
-    const int col = rem >> 5, rp = rem & 31;
-    const double* src = (pp & 1) ? Y : X;
+// Issue the cp.async copies of one pipeline stage: panels of tile (ti, tj), chunk kc.
+// 4 (panel, plane) x 32 columns x 32 row-pairs = 4096 16-byte copies, 16 per thread;
+// thread tid copies row-pair rp = tid & 31 of columns 8*(i & 3) + (tid >> 5), plane-panel
+// i >> 2 (i = 0..15), so all index math is per-thread constants plus one chunk offset.
+__device__ __forceinline__ void load_stage(const double* X, const double* Y, int da, int ti, int tj,
+                                           int kc, double* stage, int tid) {
+  const int rp = tid & 31, c0 = tid >> 5;
+  const double* srcA = nullptr;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int pp = i >> 2, col = 8 * (i & 3) + c0;
+    srcA = (pp & 1) ? Y : X;
     const int row0 = ((pp >> 1) ? tj : ti) * TB;
-    const double* g = src + (row0 + 2 * rp) + static_cast<size_t>(kc * KC + col) * G.da;
-    double* s = stage + pp * kPanel + col * SP + 2 * rp;
-    cp_async16(s, g);
+    const double* g = srcA + (row0 + 2 * rp) + static_cast<size_t>(kc * KC + col) * da;
+    cp_async16(stage + pp * kPanel + col * SP + 2 * rp, g);
   }
 }
 
-// rho partials over all tiles of Psi' (X, Y planes in global memory).
+// rho partials of the tiles t = first, first + stride, ... (rank's share), as two chains by
+// tile parity: out = {rho2_even, rho2_odd, tr_even, tr_odd}, warp-reduced (all lanes).
+// inject_fault flips the sign of the first accumulation term of rho(0,0) (linalg.cpp:94)
+// after the trace is taken.
 __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, const double* Y,
                                              double* stages, int tid, int warp, int lane,
-                                             bool fault, double& rho2_out, double& tr_out) {
+                                             int first, int stride, bool fault, double out[4]) {
   const int wr = warp / T8::WC, wc = warp % T8::WC;
   const int m = lane >> 2, kq = lane & 3;
   const int nk = G.kchunks(), nt = G.tiles();
-  const int total = nt * nt * nk;
+  const int mine = (nt * nt - first + stride - 1) / stride;
+  const int total = mine * nk;
   double cr[2][4][2], ci[2][4][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-  double rho2 = 0.0, tr = 0.0;
-
-  load_stage(G, X, Y, 0, stages, tid);
-  cp_async_commit();
-  for (int it = 0; it < total; ++it) {
-    if (it + 1 < total) {
-      load_stage(G, X, Y, it + 1, stages + ((it + 1) & 1) * kStage, tid);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+  double rho[2] = {0.0, 0.0}, tr[2] = {0.0, 0.0};
+  auto issue = [&](int it) {
+    if (it < total) {
+      const int t = first + (it / nk) * stride, kc = it % nk;
+      load_stage(X, Y, G.da, t / nt, t % nt, kc, stages + (it % kStages) * kStage, tid);
     }
-    consumer_sync(kConsumers);
-    const double* st = stages + (it & 1) * kStage;
+    cp_async_commit();  // (possibly empty) group per iteration keeps the wait counts uniform
+  };
+  issue(0);
+  issue(1);
+  for (int it = 0; it < total; ++it) {
+    cp_async_wait<1>();       // this thread's copies of stage `it` landed
+    consumer_sync(kThreads);  // everyone's did; stage (it-1) % 3 is free
+    issue(it + 2);
+    const double* st = stages + (it % kStages) * kStage;
     const double *AX = st, *AY = st + kPanel, *BX = st + 2 * kPanel, *BY = st + 3 * kPanel;
 #pragma unroll
     for (int kb = 0; kb < KC; kb += 4) {
@@ -149,37 +167,41 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
           dmma(ci[i][j][0], ci[i][j][1], xn[i], yb[j]);
         }
     }
-    const int kc = it % nk;
-    if (kc == nk - 1) {  // tile epilogue
-      const int tile = it / nk, ti = tile / nt, tj = tile % nt;
+    if (it % nk == nk - 1) {  // tile epilogue
+      const int t = first + (it / nk) * stride, ti = t / nt, tj = t % nt, c = t & 1;
       if (ti == tj) {
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             if (wr * 2 + i == wc * 4 + j) {
-              if (m == 2 * kq) tr += cr[i][j][0];
-              if (m == 2 * kq + 1) tr += cr[i][j][1];
+              if (m == 2 * kq) tr[c] += cr[i][j][0];
+              if (m == 2 * kq + 1) tr[c] += cr[i][j][1];
             }
       }
-      if (fault && tile == 0 && wr == 0 && wc == 0 && lane == 0)
+      if (fault && t == 0 && wr == 0 && wc == 0 && lane == 0)
         cr[0][0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);
+      double acc = rho[c];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            rho2 = fma(cr[i][j][e], cr[i][j][e], rho2);
-            rho2 = fma(ci[i][j][e], ci[i][j][e], rho2);
+            acc = fma(cr[i][j][e], cr[i][j][e], acc);
+            acc = fma(ci[i][j][e], ci[i][j][e], acc);
             cr[i][j][e] = 0.0;
             ci[i][j][e] = 0.0;
           }
+      rho[c] = acc;
     }
-    consumer_sync(kConsumers);  // stage (it&1) free for iteration it+2
   }
-  rho2_out = warp_sum(rho2);
-  tr_out = warp_sum(tr);
+  cp_async_wait<0>();
+  out[0] = warp_sum(rho[0]);
+  out[1] = warp_sum(rho[1]);
+  out[2] = warp_sum(tr[0]);
+  out[3] = warp_sum(tr[1]);
+  consumer_sync(kThreads);  // all warps done with the stages before they are reused
 }
 
 cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const double* u,

@@ -27,7 +27,8 @@ struct AnnealParams {
   double* final_entropy;
   int32_t* status;
   int64_t* status_step;
-  double* workspace;  // HBM tier: per-CTA psi/psi' slabs; TRACE probe: phase stamps
+  double* workspace;  // HBM tier: per-CTA psi/psi' slabs
+  int64_t* trace;     // phase-trace probe only: clock64 stamps [steps][8] of CTA 0's first row
   const GateRec* gates;        // [rows][steps] proposal stream (gate_stream.cu)
   const double* init_states;   // [rows][2^S] interleaved, unnormalised (random start) or null
 };
@@ -50,7 +51,8 @@ constexpr int kSmemMaxSpins = 12;
 cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* grid_out,
                                bool trace = false);
 // anneal_hbm.cu (S >= 13)
-cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out);
+cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out,
+                              bool trace = false);
 size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device);
 
 // probes.cu

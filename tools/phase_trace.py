@@ -17,6 +17,8 @@ spins = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 replicas = int(sys.argv[2]) if len(sys.argv) > 2 else 148
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 200
 t = tg.probe_phase_trace(spins, replicas, steps).astype(np.float64)
+if steps < 14:
+    raise SystemExit("need >= 14 steps")
 s, nxt = t[10:-2], t[11:-1]
 rows = {
     "step": nxt[:, 0] - s[:, 0],
