@@ -105,7 +105,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_reference_sample(cfg_spins, replicas, mc_steps, threads, target_s=15.0):
+def cpu_reference_sample(cfg_spins, replicas, mc_steps, threads, target_s=15.0, entropy_kind=1):
     """Time the reference's own CPU path (oracle/_ref: spinmc::mc_procedure + DirectExecutor,
     pooled host threads) on a bounded sample; falls back to the oracle port if _ref is absent."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -117,14 +117,14 @@ def cpu_reference_sample(cfg_spins, replicas, mc_steps, threads, target_s=15.0):
     cal_steps = 20
     t0 = time.perf_counter()
     if kind == "reference":
-        lib.run(McCfg(spins=cfg_spins, steps=cal_steps), 0, 1, threads=1, sites=False)
+        lib.run(McCfg(spins=cfg_spins, steps=cal_steps, entropy_kind=entropy_kind), 0, 1, threads=1, sites=False)
     else:
-        lib.run(McCfg(spins=cfg_spins, steps=cal_steps), 0, 1, threads=1)
+        lib.run(McCfg(spins=cfg_spins, steps=cal_steps, entropy_kind=entropy_kind), 0, 1, threads=1)
     per_step = max((time.perf_counter() - t0) / cal_steps, 1e-7)
     # sample: `threads*2` replicas (or fewer), steps chosen for ~target_s of wall time
     n_rep = int(min(replicas, max(threads * 2, 1)))
     steps = int(max(5, min(mc_steps, target_s * threads / (per_step * n_rep))))
-    cfg = McCfg(spins=cfg_spins, steps=steps)
+    cfg = McCfg(spins=cfg_spins, steps=steps, entropy_kind=entropy_kind)
     t0 = time.perf_counter()
     if kind == "reference":
         lib.run(cfg, 0, n_rep, threads=threads, sites=False)
@@ -144,7 +144,8 @@ def run_reference_arm(args, cfgw, rank, world):
     vals = []
     for i in range(args.warmup + args.steps):
         cb, wall = cpu_reference_sample(cfgw["spins"], cfgw["replicas"], cfgw["mc_steps"], threads,
-                                        target_s=args.ref_seconds)
+                                        target_s=args.ref_seconds,
+                                        entropy_kind=0 if args.entropy == "von-neumann" else 1)
         if i >= args.warmup:
             vals.append(cb["value"])
     value = float(np.median(vals))
@@ -160,12 +161,15 @@ def run_reference_arm(args, cfgw, rank, world):
     return 0
 
 
-def load_traffic(spins):
+def load_traffic(spins, rows, mc_steps):
+    """DRAM bytes per anneal-kernel launch of this exact workload from a committed ncu --set
+    full capture (profiles/ncu_traffic.json), or None when no capture of it exists."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(str(spins))
-    except (OSError, ValueError):
+            ent = json.load(f).get(f"{spins}x{rows}x{mc_steps}")
+        return None if ent is None else float(ent["bytes"])
+    except (OSError, ValueError, KeyError, TypeError):
         return None
 
 
@@ -180,6 +184,8 @@ def main():
     ap.add_argument("--replicas", type=int, default=None, help="replicas per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--entropy", choices=["renyi-2", "von-neumann"], default="renyi-2",
+                    help="entropy kind (BASELINE metric is quoted on renyi-2, the bench default)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: W >= 3
@@ -221,7 +227,7 @@ def main():
 
     spins, R, S = cfgw["spins"], cfgw["replicas"], cfgw["mc_steps"]
     procedures = R * world
-    cfg = tg.ExperimentConfig(spins=spins, steps=S, procedures=procedures, seed=0,
+    cfg = tg.ExperimentConfig(spins=spins, steps=S, procedures=procedures, seed=0, entropy_kind=args.entropy,
                               shard_index=rank, shard_count=world)
     ccfg = cfg.to_c()
     rows = cfg.rows()
@@ -257,6 +263,7 @@ def main():
 
     # ------------------------------------------------------------ timed: device-resident
     times = []
+    launches0 = tg.kernel_launches()
     with ClockSampler(local_rank) as clocks:
         for _ in range(args.steps):
             flush.fill_(1.0)  # L2 flush (256 MiB > 126 MB L2), outside the timed interval
@@ -271,6 +278,7 @@ def main():
             barrier()
             times.append(e0.elapsed_time(e1) / 1e3)
     clk = clocks.summary()
+    launches = tg.kernel_launches() - launches0  # ours only (torch's L2-flush fill excluded)
     t_step = max_over_ranks(float(np.mean(times)))
     replica_steps = procedures * S
     value = replica_steps / t_step
@@ -303,7 +311,8 @@ def main():
 
     cpu_baseline = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu_baseline, _ = cpu_reference_sample(spins, R, S, os.cpu_count() or 1)
+        cpu_baseline, _ = cpu_reference_sample(spins, R, S, os.cpu_count() or 1,
+                                               entropy_kind=0 if args.entropy == "von-neumann" else 1)
 
     if rank == 0:
         line = {
@@ -312,7 +321,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded product states, seed 0)",
             "config": {"workload": cfgw["name"], "spins": spins, "gemm_mnk": [tg.dims_for_spins(spins)[0]] * 2 + [tg.dims_for_spins(spins)[1]], "replicas_per_gpu": R, "procedures": procedures,
                        "mc_steps": S, "parallelism": f"dp{world} (replica p on GPU p mod {world})",
-                       "entropy": "renyi-2", "l2": "flushed between timed iterations (256 MiB write)"},
+                       "entropy": args.entropy, "l2": "flushed between timed iterations (256 MiB write)"},
             "tflops": replica_steps * tg.step_flops(spins) / t_step / 1e12,
             "average_entropy": avg, "best_procedure": best, "best_entropy": best_e,
             "roofline": {"bound": "tensor", "kernel": "anneal_smem_kernel" if spins <= 12 else "anneal_hbm_kernel",
@@ -320,10 +329,10 @@ def main():
                          "frac": achieved / peak_tflops,
                          "peak_source": f"live DMMA.8x8x4 probe (tg_fp64_dmma_peak, {peak_clock:.3f} GHz); "
                                         "MEASURED_PEAKS.json has no FP64 entry; see profiles/r01_fp64_peak.json",
-                         "flops_per_launch": flops_launch, "traffic": load_traffic(spins)},
+                         "timed": "tg_anneal_launch on its stream (proposal pre-pass ~2% + anneal kernel), CUDA events", "flops_per_launch": flops_launch, "traffic": load_traffic(spins, rows, S)},
             "e2e": {"value": replica_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": C.sizeof(ccfg),
                     "d2h_bytes_per_step": d2h * world, "ms_per_step": t_e2e * 1e3},
-            "gpu_launches": args.steps * world,
+            "gpu_launches": launches * world,
             "clocks": clk,
             "cpu_baseline": cpu_baseline,
         }

@@ -96,6 +96,9 @@ typedef struct {
 
 const char* tg_last_error(void);
 const char* tg_version(void);
+// Number of CUDA kernels this library has launched in this process (anneal pipeline and
+// batched GEMM; probes excluded). Lets a caller count launches inside a timed region.
+uint64_t tg_kernel_launches(void);
 
 /* Opens a context over `n` GPUs (device ordinals; NULL = 0..n-1). Owns streams and
  * device buffers. One caller per context at a time (documented). */
@@ -167,6 +170,10 @@ tg_status tg_probe_apply_gate(uint32_t spins, const double* psi, int site, const
  * norms receives ||psi|| (may be NULL) */
 tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* entropy,
                            double* norms);
+/* same with the entropy kind (tg_entropy_kind): TG_VON_NEUMANN = eigenvalues of rho on the
+ * device (spins <= 12), spinmc.cpp:165-169 / linalg.cpp:161-232 */
+tg_status tg_probe_entropy_kind(uint32_t spins, uint64_t count, const double* psi, int32_t kind,
+                                double* entropy, double* norms);
 
 /* Profiling probe: runs `replicas` replicas and returns clock64 phase stamps of CTA 0's
  * first replica, trace[steps][8]: 0 step start, 1 gate pass done, 2 GEMM done,

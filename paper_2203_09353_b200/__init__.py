@@ -96,11 +96,11 @@ class CKernelRecord(C.Structure):
 
 # Every symbol declared in include/taskgemm_b200.h (checked by tests/test_capi_symbols.py).
 EXPORTS = [
-    "tg_last_error", "tg_version", "tg_create", "tg_shutdown", "tg_destroy", "tg_validate",
+    "tg_last_error", "tg_version", "tg_kernel_launches", "tg_create", "tg_shutdown", "tg_destroy", "tg_validate",
     "tg_anneal_rows", "tg_step_flops", "tg_anneal_run", "tg_anneal_launch",
     "tg_anneal_workspace_bytes", "tg_zgemm_batched", "tg_zgemm_strided_launch",
     "tg_fp64_dmma_peak", "tg_probe_rng", "tg_probe_gates", "tg_probe_apply_gate",
-    "tg_probe_entropy", "tg_probe_phase_trace", "tg_set_perturb_gemm",
+    "tg_probe_entropy", "tg_probe_entropy_kind", "tg_probe_phase_trace", "tg_set_perturb_gemm",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -119,6 +119,7 @@ def lib() -> C.CDLL:
     L = C.CDLL(LIB_PATH)
     L.tg_last_error.restype = C.c_char_p
     L.tg_version.restype = C.c_char_p
+    L.tg_kernel_launches.restype = C.c_uint64
     L.tg_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
     L.tg_shutdown.argtypes = [C.c_void_p]
     L.tg_destroy.argtypes = [C.c_void_p]
@@ -142,10 +143,11 @@ def lib() -> C.CDLL:
     L.tg_probe_gates.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _u8p, _dp, _dp]
     L.tg_probe_apply_gate.argtypes = [C.c_uint32, _dp, C.c_int, _dp, _dp]
     L.tg_probe_entropy.argtypes = [C.c_uint32, C.c_uint64, _dp, _dp, _dp]
+    L.tg_probe_entropy_kind.argtypes = [C.c_uint32, C.c_uint64, _dp, C.c_int32, _dp, _dp]
     L.tg_set_perturb_gemm.argtypes = [C.c_int]
     L.tg_probe_phase_trace.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64)]
     for name in EXPORTS:
-        if name not in ("tg_last_error", "tg_version", "tg_anneal_rows", "tg_step_flops",
+        if name not in ("tg_last_error", "tg_version", "tg_kernel_launches", "tg_anneal_rows", "tg_step_flops",
                         "tg_anneal_workspace_bytes"):
             getattr(L, name).restype = C.c_int
     _lib = L
@@ -405,12 +407,16 @@ def probe_apply_gate(spins: int, psi: np.ndarray, site: int, u: np.ndarray) -> n
     return out
 
 
-def probe_entropy(spins: int, states: np.ndarray):
+def probe_entropy(spins: int, states: np.ndarray, kind: str = "renyi-2"):
+    """Device entropy (and ||psi||) of host states [count, 2^spins] through the anneal
+    kernels' rho path; kind "renyi-2" or "von-neumann"."""
+    if kind not in _ENTROPY:
+        raise ConfigError(f"unknown entropy_kind: {kind!r}")
     states = np.ascontiguousarray(states, np.complex128).reshape(-1, 1 << spins)
     e = np.zeros(states.shape[0])
     n = np.zeros(states.shape[0])
-    _check(lib().tg_probe_entropy(spins, states.shape[0], states.ctypes.data_as(_dp), e.ctypes.data_as(_dp),
-                                  n.ctypes.data_as(_dp)))
+    _check(lib().tg_probe_entropy_kind(spins, states.shape[0], states.ctypes.data_as(_dp), _ENTROPY[kind],
+                                       e.ctypes.data_as(_dp), n.ctypes.data_as(_dp)))
     return e, n
 
 
@@ -419,6 +425,11 @@ def probe_phase_trace(spins: int, replicas: int, steps: int) -> np.ndarray:
     out = np.zeros((steps, 8), np.int64)
     _check(lib().tg_probe_phase_trace(spins, replicas, steps, out.ctypes.data_as(C.POINTER(C.c_int64))))
     return out
+
+
+def kernel_launches() -> int:
+    """Kernels the library has launched in this process (tg_kernel_launches)."""
+    return int(lib().tg_kernel_launches())
 
 
 def fp64_dmma_peak(device: int = 0) -> tuple[float, float]:

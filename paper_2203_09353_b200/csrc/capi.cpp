@@ -83,9 +83,11 @@ tg_status validate(const tg_anneal_config* c) {
   if (c->spins > 24)
     return fail(TG_EINVAL, "device tiers cover spins <= 24 (state of 2^" + std::to_string(c->spins) +
                                " amplitudes per replica)");
-  if (c->entropy_kind != TG_RENYI2)
-    return fail(TG_EINVAL,
-                "device path computes renyi-2 entropy only (von-neumann is the next row, DESIGN.md)");
+  if (c->entropy_kind != TG_RENYI2 && c->entropy_kind != TG_VON_NEUMANN)
+    return fail(TG_ECONFIG, "entropy_kind must be von-neumann or renyi-2");
+  if (c->entropy_kind == TG_VON_NEUMANN && c->spins > static_cast<uint32_t>(tg::kVnMaxSpins))
+    return fail(TG_EINVAL, "device von-neumann entropy covers spins <= " + std::to_string(tg::kVnMaxSpins) +
+                               " (rho resident in shared memory); use renyi-2");
   if (c->objective != TG_MAXIMIZE && c->objective != TG_MINIMIZE)
     return fail(TG_ECONFIG, "objective must be max or min");
   if (c->initial_state != TG_PRODUCT && c->initial_state != TG_RANDOM)
@@ -101,6 +103,7 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
   p.objective = c->objective;
   p.initial_state = c->initial_state;
   p.inject_fault = c->inject_fault || g_perturb.load();
+  p.entropy_kind = c->entropy_kind;
   p.steps = c->steps;
   p.seed = c->seed;
   p.renorm = c->renormalize_interval;
@@ -127,6 +130,9 @@ size_t workspace_for(const tg::AnnealParams& p, int device) {
   const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(p.rows, kStreamBudget / per_row));
   return batch * per_row + slab_bytes(p.spins, batch, device) + 1024;
 }
+
+// Kernels this library has launched (process lifetime): tg_kernel_launches().
+std::atomic<uint64_t> g_launches{0};
 
 // The whole device pipeline of one launch, on one stream: per batch of replicas, the
 // proposal-stream pre-pass (gate_stream.cu) then the persistent anneal kernel.
@@ -158,12 +164,14 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
     tg::GateStream gs{};
     cudaError_t e = tg::launch_gate_stream(q, base, stream_bytes, &gs, s);
     if (e != cudaSuccess) return e;
+    g_launches += p.initial_state == 1 ? 3 : 2;  // rng_draws, gate_convert (, init_convert)
     q.gates = gs.recs;
     q.init_states = gs.init_states;
     q.workspace = reinterpret_cast<double*>(slabs);
     e = p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::launch_anneal_smem(q, s, nullptr, trace)
                                                            : tg::launch_anneal_hbm(q, s, nullptr, trace);
     if (e != cudaSuccess) return e;
+    ++g_launches;
   }
   return cudaSuccess;
 }
@@ -186,6 +194,8 @@ size_t trace_bytes(uint64_t rows, uint64_t steps, bool sites, bool wall) {
 extern "C" {
 
 const char* tg_last_error(void) { return g_err.c_str(); }
+uint64_t tg_kernel_launches(void) { return g_launches.load(); }
+
 const char* tg_version(void) { return "taskgemm-b200 0.1 (sm_100a, DMMA.8x8x4 persistent anneal)"; }
 
 uint64_t tg_anneal_rows(const tg_anneal_config* cfg) { return cfg ? rows_for(cfg) : 0; }
@@ -427,6 +437,7 @@ tg_status tg_zgemm_strided_launch(int batch, int m, int n, int k, const double a
                                            beta[1], C, sC, out, sO, inject_fault || g_perturb.load(),
                                            static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "zgemm launch");
+  ++g_launches;
   return TG_OK;
 }
 
@@ -462,6 +473,7 @@ tg_status tg_zgemm_batched(tg_ctx* ctx, int device, int batch, int m, int n, int
                                            beta[0], beta[1], dC, ec / 2, dO, ec / 2, g_perturb.load(),
                                            d.stream);
   if (e != cudaSuccess) return cuda_fail(e, "zgemm launch");
+  ++g_launches;
   TG_CUDA(cudaEventRecord(d.ev1, d.stream));
   for (int i = 0; i < batch; ++i)
     TG_CUDA(cudaMemcpyAsync(out[i], dO + i * ec, 8 * ec, cudaMemcpyDeviceToHost, d.stream));
@@ -548,21 +560,30 @@ tg_status tg_probe_apply_gate(uint32_t spins, const double* psi, int site, const
   return TG_OK;
 }
 
-tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* entropy,
-                           double* norms) {
+tg_status tg_probe_entropy_kind(uint32_t spins, uint64_t count, const double* psi, int32_t kind,
+                                double* entropy, double* norms) {
   if (spins < 2 || spins > 24) return fail(TG_EINVAL, "probe_entropy: spins must be in [2,24]");
+  if (kind != TG_RENYI2 && kind != TG_VON_NEUMANN) return fail(TG_ECONFIG, "probe_entropy: unknown entropy kind");
+  if (kind == TG_VON_NEUMANN && spins > static_cast<uint32_t>(tg::kVnMaxSpins))
+    return fail(TG_EINVAL, "probe_entropy: device von-neumann covers spins <= " + std::to_string(tg::kVnMaxSpins));
   if (count < 1) return TG_OK;
   const size_t n = size_t{1} << spins;
   double* d = nullptr;
   TG_CUDA(cudaMalloc(&d, 8 * (2 * n * count + 2 * count)));
   double *dp = d, *de = d + 2 * n * count, *dn = de + count;
   cudaError_t e = cudaMemcpy(dp, psi, 16 * n * count, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = tg::probe_entropy(spins, count, dp, de, dn, g_perturb.load() != 0, nullptr);
+  if (e == cudaSuccess)
+    e = tg::probe_entropy(spins, count, dp, de, dn, g_perturb.load() != 0, nullptr, kind == TG_VON_NEUMANN);
   if (e == cudaSuccess) e = cudaMemcpy(entropy, de, 8 * count, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess && norms) e = cudaMemcpy(norms, dn, 8 * count, cudaMemcpyDeviceToHost);
   cudaFree(d);
   if (e != cudaSuccess) return cuda_fail(e, "probe_entropy");
   return TG_OK;
+}
+
+tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* entropy,
+                           double* norms) {
+  return tg_probe_entropy_kind(spins, count, psi, TG_RENYI2, entropy, norms);
 }
 
 tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* trace) {

@@ -4,6 +4,7 @@
 #include "hbm_tier.cuh"
 #include "smem_tier.cuh"
 #include "tg_internal.h"
+#include "vn.cuh"
 
 namespace tg {
 namespace {
@@ -88,6 +89,33 @@ __global__ void entropy_smem_kernel(const double* psi_all, double* e_out, double
   }
 }
 
+// von Neumann entropy of each state (vn.cuh), same rho path as the anneal kernel.
+template <int LA, int LB>
+__global__ void entropy_vn_smem_kernel(const double* psi_all, double* e_out, double* n_out, bool fault) {
+  using D = smem::Dims<LA, LB>;
+  constexpr int RP = D::DA_PAD + 1;
+  extern __shared__ __align__(128) unsigned char raw[];
+  __shared__ double part[smem::kConsumerWarps];
+  double* planes = reinterpret_cast<double*>(raw);
+  double* Rr = planes + 2 * D::PLANE;
+  double* Ri = Rr + D::DA_PAD * RP;
+  vn::Scratch& W = *reinterpret_cast<vn::Scratch*>(Ri + D::DA_PAD * RP);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const double* psi = psi_all + 2ull * D::N * blockIdx.x;
+  load_state<D>(psi, planes, planes + D::PLANE, tid, blockDim.x);
+  double rho2, tr;
+  smem::rho_partials<D, true>(planes, planes + D::PLANE, warp, lane, fault, rho2, tr, Rr, Ri, RP);
+  if (lane == 0) part[warp] = tr;
+  __syncthreads();
+  const double e = vn::entropy(Rr, Ri, D::DA, RP, W, tid, [] { __syncthreads(); });
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < smem::kConsumerWarps; ++w) t += part[w];
+    e_out[blockIdx.x] = e;
+    if (n_out) n_out[blockIdx.x] = __dsqrt_rn(t);
+  }
+}
+
 template <int S>
 cudaError_t gate_s(const double* psi, int site, const double* u, double* out, cudaStream_t s) {
   constexpr int LA = S / 2, LB = S - S / 2;
@@ -101,9 +129,16 @@ cudaError_t gate_s(const double* psi, int site, const double* u, double* out, cu
 
 template <int S>
 cudaError_t entropy_s(uint64_t count, const double* psi, double* e, double* n, bool fault,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool von_neumann) {
   constexpr int LA = S / 2, LB = S - S / 2;
   using D = smem::Dims<LA, LB>;
+  if (von_neumann) {
+    const int bytes = 2 * D::PLANE * 8 + 2 * D::DA_PAD * (D::DA_PAD + 1) * 8 + static_cast<int>(sizeof(vn::Scratch));
+    auto k = entropy_vn_smem_kernel<LA, LB>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    k<<<static_cast<unsigned>(count), smem::kConsumers, bytes, s>>>(psi, e, n, fault);
+    return cudaGetLastError();
+  }
   const int bytes = 2 * D::PLANE * 8;
   auto k = entropy_smem_kernel<LA, LB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -183,19 +218,20 @@ cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const 
 }
 
 cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* e,
-                          double* n, bool fault, cudaStream_t s) {
+                          double* n, bool fault, cudaStream_t s, bool von_neumann) {
+  if (von_neumann && spins > static_cast<uint32_t>(kVnMaxSpins)) return cudaErrorInvalidValue;
   switch (spins) {
-    case 2: return entropy_s<2>(count, psi, e, n, fault, s);
-    case 3: return entropy_s<3>(count, psi, e, n, fault, s);
-    case 4: return entropy_s<4>(count, psi, e, n, fault, s);
-    case 5: return entropy_s<5>(count, psi, e, n, fault, s);
-    case 6: return entropy_s<6>(count, psi, e, n, fault, s);
-    case 7: return entropy_s<7>(count, psi, e, n, fault, s);
-    case 8: return entropy_s<8>(count, psi, e, n, fault, s);
-    case 9: return entropy_s<9>(count, psi, e, n, fault, s);
-    case 10: return entropy_s<10>(count, psi, e, n, fault, s);
-    case 11: return entropy_s<11>(count, psi, e, n, fault, s);
-    case 12: return entropy_s<12>(count, psi, e, n, fault, s);
+    case 2: return entropy_s<2>(count, psi, e, n, fault, s, von_neumann);
+    case 3: return entropy_s<3>(count, psi, e, n, fault, s, von_neumann);
+    case 4: return entropy_s<4>(count, psi, e, n, fault, s, von_neumann);
+    case 5: return entropy_s<5>(count, psi, e, n, fault, s, von_neumann);
+    case 6: return entropy_s<6>(count, psi, e, n, fault, s, von_neumann);
+    case 7: return entropy_s<7>(count, psi, e, n, fault, s, von_neumann);
+    case 8: return entropy_s<8>(count, psi, e, n, fault, s, von_neumann);
+    case 9: return entropy_s<9>(count, psi, e, n, fault, s, von_neumann);
+    case 10: return entropy_s<10>(count, psi, e, n, fault, s, von_neumann);
+    case 11: return entropy_s<11>(count, psi, e, n, fault, s, von_neumann);
+    case 12: return entropy_s<12>(count, psi, e, n, fault, s, von_neumann);
     default: return hbm::probe_entropy(spins, count, psi, e, n, fault, s);
   }
 }

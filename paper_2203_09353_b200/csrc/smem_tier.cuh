@@ -100,10 +100,13 @@ __device__ __forceinline__ void gate_pass_fma(const double* __restrict__ sx,
 // Per-warp sum |rho_ij|^2 and trace(rho) of rho = Psi Psi^dagger (warp-reduced; valid in
 // every lane). inject_fault flips the sign of the first accumulation term of rho(0,0)
 // (linalg.cpp:94 testhook) AFTER the trace is taken, so only the entropy is corrupted.
-template <class D>
+// STORE (von Neumann): rho is also written to planar SMEM Rr/Ri (column-major, pitch RP).
+template <class D, bool STORE = false>
 __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
                                              const double* __restrict__ Y, int warp, int lane,
-                                             bool fault, double& rho2, double& trace) {
+                                             bool fault, double& rho2, double& trace,
+                                             double* Rr = nullptr, double* Ri = nullptr,
+                                             int RP = 0) {
   using T = Tile<D::NB>;
   rho2 = 0.0;
   trace = 0.0;
@@ -160,6 +163,11 @@ __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
         for (int e = 0; e < 2; ++e) {
           rho2 = fma(cr[i][j][e], cr[i][j][e], rho2);
           rho2 = fma(ci[i][j][e], ci[i][j][e], rho2);
+          if constexpr (STORE) {
+            const int o = (wr * T::TM + i) * 8 + m + ((wc * T::TN + j) * 8 + 2 * kq + e) * RP;
+            Rr[o] = cr[i][j][e];
+            Ri[o] = ci[i][j][e];
+          }
         }
   }
   rho2 = warp_sum(rho2);

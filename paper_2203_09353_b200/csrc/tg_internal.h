@@ -16,6 +16,7 @@ struct AnnealParams {
   int32_t objective;      // 0 maximize, 1 minimize
   int32_t initial_state;  // 0 product, 1 random
   int32_t inject_fault;
+  int32_t entropy_kind;   // 0 von Neumann, 1 Renyi-2 (tg_entropy_kind)
   uint64_t steps, seed, renorm;
   double t0, t_min;
   uint64_t rows, p_first, p_stride;
@@ -46,6 +47,7 @@ cudaError_t launch_gate_stream(const AnnealParams& p, void* ws, size_t ws_bytes,
 enum : int32_t { kRowOk = 0, kRowNotNormalized = 2 };
 
 constexpr int kSmemMaxSpins = 12;
+constexpr int kVnMaxSpins = 12;  // device von Neumann (vn.cuh): d_a <= 64, SMEM tier
 
 // anneal_smem.cu (S <= 12)
 cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* grid_out,
@@ -62,7 +64,7 @@ cudaError_t probe_gates(uint32_t spins, uint64_t seed, uint64_t p, uint64_t step
 cudaError_t probe_apply_gate(uint32_t spins, const double* d_psi, int site, const double* d_u,
                              double* d_out, cudaStream_t s);
 cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* d_psi, double* d_e,
-                          double* d_norm, bool fault, cudaStream_t s);
+                          double* d_norm, bool fault, cudaStream_t s, bool von_neumann = false);
 cudaError_t fp64_dmma_peak(double* tflops, double* clock_ghz);
 
 // zgemm.cu

@@ -6,7 +6,7 @@ import math
 
 import numpy as np
 import pytest
-from conftest import TRAJ_CASES, load_traj
+from conftest import TRAJ_CASES, VN_CASES, entropy_kind_of, load_traj
 from oracle_lib import McCfg
 
 import paper_2203_09353_b200 as tg
@@ -88,6 +88,47 @@ def test_t5_rho_entropy_vs_reference(kats, spins):
     assert np.abs(n - 1.0).max() <= 1e-13
 
 
+@pytest.mark.parametrize("spins", [2, 3, 4, 6, 8, 9, 12])
+def test_t5_von_neumann_vs_reference(kats, oracle, spins):
+    """Device eigen-solver (vn.cuh: Householder + Sturm multisection) against the reference's
+    cyclic Jacobi (linalg.cpp:161-232) on the golden states (the oracle's bitwise restatement
+    where the fixture has no vN values)."""
+    states = kats[f"ent_{spins}_states"]
+    want = kats[f"ent_{spins}_vn"]
+    if want.size == 0:
+        want = np.array([oracle.entropy(spins, s, 0) for s in states])
+    e, n = tg.probe_entropy(spins, states, kind="von-neumann")
+    assert close(e, want).all(), np.max(np.abs(e - want))
+    assert np.abs(n - 1.0).max() <= 1e-13
+
+
+@pytest.mark.parametrize("spins", [5, 7, 10, 11, 12])
+def test_t5_von_neumann_structured_states(oracle, spins):
+    """Spectra the annealer produces: product states (rank 1), low Schmidt rank with
+    degenerate and tiny (<1e-15, dropped) eigenvalues, and Haar-random (full rank)."""
+    rng = np.random.default_rng(7 * spins)
+    da, db = 1 << (spins // 2), 1 << (spins - spins // 2)
+    states = []
+    for rank, weights in [(1, None), (2, [0.5, 0.5]), (3, [0.6, 0.4 - 1e-16, 1e-16]), (4, None),
+                          (da, None), (da, "geometric")]:
+        a = np.linalg.qr(rng.standard_normal((da, da)) + 1j * rng.standard_normal((da, da)))[0][:, :rank]
+        b = np.linalg.qr(rng.standard_normal((db, db)) + 1j * rng.standard_normal((db, db)))[0][:, :rank]
+        if weights is None:
+            w = rng.random(rank)
+        elif weights == "geometric":
+            w = 0.5 ** np.arange(rank)
+        else:
+            w = np.array(weights)
+        w = np.sqrt(w / w.sum())
+        Psi = (a * w) @ b.T
+        psi = Psi.T.reshape(-1)  # psi[a + b*d_a] = Psi[a, b]
+        states.append(psi / np.linalg.norm(psi))
+    states = np.array(states)
+    e, _ = tg.probe_entropy(spins, states, kind="von-neumann")
+    want = np.array([oracle.entropy(spins, s, 0) for s in states])
+    assert close(e, want).all(), np.max(np.abs(e - want))
+
+
 @pytest.mark.parametrize("spins", [16, 18])
 def test_t5_rho_entropy_large(oracle, spins):
     rng = np.random.default_rng(100 + spins)
@@ -148,7 +189,8 @@ def cfg_from(g, procedures=None):
         spins=int(g["spins"]), steps=int(g["steps"]), procedures=procedures or int(g["procedures"]),
         seed=int(g["seed"]), objective="max" if int(g["objective"]) == 0 else "min",
         initial_state="product" if int(g["initial_state"]) == 0 else "random",
-        t0=float(g["t0"]), t_min=float(g["t_min"]), renormalize_interval=int(g["renorm"]))
+        t0=float(g["t0"]), t_min=float(g["t_min"]), renormalize_interval=int(g["renorm"]),
+        entropy_kind="renyi-2" if entropy_kind_of(g) == 1 else "von-neumann")
 
 
 def assert_traj_parity(rep, g, rows=None):
@@ -168,6 +210,20 @@ def test_t7_trajectory_parity(device, name):
     assert_traj_parity(rep, g)
     assert abs(rep.average_entropy - float(g["average"])) <= TOL * max(1.0, abs(float(g["average"])))
     assert rep.total_flops == (rep.entropies.size + rep.initial_entropy.size) * tg.step_flops(int(g["spins"]))
+
+
+@pytest.mark.parametrize("name", VN_CASES)
+def test_t7_von_neumann_trajectory_parity(device, name):
+    g = load_traj(name)
+    rep = device.run(cfg_from(g))
+    assert_traj_parity(rep, g)
+    assert abs(rep.average_entropy - float(g["average"])) <= TOL * max(1.0, abs(float(g["average"])))
+
+
+def test_t7_von_neumann_appendix_a(device):
+    rep = device.run(cfg_from(load_traj("vn_cfg1")))
+    assert int(rep.accepted.sum()) == 59795
+    assert abs(rep.average_entropy - 2.360208109374111) <= 1e-10 * 2.37
 
 
 def test_t7_config1_appendix_a(device):

@@ -1,7 +1,8 @@
 """Generate tests/golden/*.npz from the REFERENCE itself (oracle/_ref/libtgref.so, built by
 `make -C oracle ref` from /root/reference/proj/src). Run in the build container:
 
-    python tools/make_golden.py
+    python tools/make_golden.py             # everything
+    python tools/make_golden.py vn_cfg1 ... # only the named trajectory cases
 
 The fixtures pin the oracle restatement (oracle/oracle.c) and the device path on machines
 where /root/reference does not exist (the GPU box). Config cases follow BASELINE.json
@@ -24,6 +25,13 @@ OUT = os.path.join(ROOT, "tests", "golden")
 def main() -> None:
     os.makedirs(OUT, exist_ok=True)
     r = RefLib()
+    only = set(sys.argv[1:])
+    if not only:
+        known_answers(r)
+    trajectories(r, only)
+
+
+def known_answers(r) -> None:
     rng = np.random.default_rng(20220317)
 
     # --- RNG / Haar / gate / entropy / gemm known answers --------------------------------
@@ -70,6 +78,9 @@ def main() -> None:
     np.savez_compressed(os.path.join(OUT, "kats.npz"), u64=u64, u64_pairs=np.array(pairs, dtype=np.uint64),
                         normals=normals, haar=haar, n_gates=gi, **gates, **ent_cases, **gemm)
 
+
+
+def trajectories(r, only) -> None:
     # --- trajectories (mc_procedure through the reference's own pooled driver) -------------
     cases = {
         "cfg1": (McCfg(spins=8, steps=1000), 64),                       # BASELINE configs[0]
@@ -82,8 +93,16 @@ def main() -> None:
         "s2": (McCfg(spins=2, steps=100), 4),
         "s3": (McCfg(spins=3, steps=100), 4),
         "frozen_min_s6": (McCfg(spins=6, steps=60, objective=1, t0=1e-12, t_min=1e-12), 4),
+        # von Neumann entropy (McConfig default, spinmc.hpp:116; SURVEY App. A second line)
+        "vn_cfg1": (McCfg(spins=8, steps=1000, entropy_kind=0), 64),
+        "vn_s12": (McCfg(spins=12, steps=120, entropy_kind=0), 4),
+        "vn_rand_min_s10": (McCfg(spins=10, steps=200, entropy_kind=0, initial_state=1, objective=1), 4),
+        "vn_s3": (McCfg(spins=3, steps=200, entropy_kind=0), 4),
+        "vn_s5_renorm7": (McCfg(spins=5, steps=150, entropy_kind=0, renormalize_interval=7), 4),
     }
     for name, (cfg, n) in cases.items():
+        if only and name not in only:
+            continue
         tr, _ = r.run(cfg, 0, n)
         avg = 0.0
         for x in tr.entropies[:, -1]:  # procedure order, spinmc.cpp:259-268
@@ -95,6 +114,7 @@ def main() -> None:
         np.savez_compressed(os.path.join(OUT, f"traj_{name}.npz"), spins=cfg.spins, steps=cfg.steps,
                             seed=cfg.seed, objective=cfg.objective, initial_state=cfg.initial_state,
                             t0=cfg.t0, t_min=cfg.t_min, renorm=cfg.renormalize_interval, procedures=n,
+                            entropy_kind=cfg.entropy_kind,
                             initial=tr.initial, entropies=tr.entropies, accepted=tr.accepted, sites=tr.sites,
                             average=avg)
         print(name, "avg", repr(avg), "accepted", int(tr.accepted.sum()))
