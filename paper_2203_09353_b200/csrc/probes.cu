@@ -93,7 +93,7 @@ __global__ void entropy_smem_kernel(const double* psi_all, double* e_out, double
 template <int LA, int LB>
 __global__ void entropy_vn_smem_kernel(const double* psi_all, double* e_out, double* n_out, bool fault) {
   using D = smem::Dims<LA, LB>;
-  constexpr int RP = D::DA_PAD + 1;
+  constexpr int RP = D::DA_PAD + 4;
   extern __shared__ __align__(128) unsigned char raw[];
   __shared__ double part[smem::kConsumerWarps];
   double* planes = reinterpret_cast<double*>(raw);
@@ -133,7 +133,7 @@ cudaError_t entropy_s(uint64_t count, const double* psi, double* e, double* n, b
   constexpr int LA = S / 2, LB = S - S / 2;
   using D = smem::Dims<LA, LB>;
   if (von_neumann) {
-    const int bytes = 2 * D::PLANE * 8 + 2 * D::DA_PAD * (D::DA_PAD + 1) * 8 + static_cast<int>(sizeof(vn::Scratch));
+    const int bytes = 2 * D::PLANE * 8 + 2 * D::DA_PAD * (D::DA_PAD + 4) * 8 + static_cast<int>(sizeof(vn::Scratch));
     auto k = entropy_vn_smem_kernel<LA, LB>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     k<<<static_cast<unsigned>(count), smem::kConsumers, bytes, s>>>(psi, e, n, fault);

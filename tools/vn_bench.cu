@@ -20,7 +20,7 @@ __device__ double hash01(uint64_t x) {
 
 __global__ void __launch_bounds__(256, 1) bench(int n, int reps, long long* clk, double* ent) {
   extern __shared__ __align__(16) double sm[];
-  const int P = n + 1;
+  const int P = n + 4;
   double* Ar = sm;
   double* Ai = Ar + n * P;
   vn::Scratch& W = *reinterpret_cast<vn::Scratch*>(Ai + n * P);
@@ -57,11 +57,11 @@ __global__ void __launch_bounds__(256, 1) bench(int n, int reps, long long* clk,
     if (tid < 32) {
       for (int i = tid; i < n; i += 32) {
         const double l = W.lam[i];
-        W.pp[0][0][i] = l > 1e-15 ? l * log(l) : 0.0;
+        W.pr[0][i] = l > 1e-15 ? l * log(l) : 0.0;
       }
       __syncwarp();
       if (tid == 0)
-        for (int i = 0; i < n; ++i) e -= W.pp[0][0][i];
+        for (int i = 0; i < n; ++i) e -= W.pr[0][i];
     }
     __syncthreads();
     const long long t3 = clock64();
@@ -74,6 +74,53 @@ __global__ void __launch_bounds__(256, 1) bench(int n, int reps, long long* clk,
     for (int k = 0; k < 3; ++k) clk[k] = acc[k] / reps;
 }
 
+// Isolated pieces of one Householder step at k = 0 (m = n-1), each repeated `reps` times.
+__global__ void __launch_bounds__(256, 1) pieces(int n, int reps, long long* clk) {
+  extern __shared__ __align__(16) double sm[];
+  const int P = n + 4;
+  double* Ar = sm;
+  double* Ai = Ar + n * P;
+  vn::Scratch& W = *reinterpret_cast<vn::Scratch*>(Ai + n * P);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < n * P; i += 256) {
+    Ar[i] = hash01(i) * 1e-3;
+    Ai[i] = hash01(i + 99999) * 1e-3;
+  }
+  for (int i = tid; i < 64; i += 256) {
+    W.vr[0][i] = W.vr[1][i] = hash01(i + 7) * 1e-3;
+    W.vi[0][i] = W.vi[1][i] = hash01(i + 8) * 1e-3;
+    W.pr[0][i] = W.pr[1][i] = hash01(i + 9) * 1e-3;
+    W.pi[0][i] = W.pi[1][i] = hash01(i + 10) * 1e-3;
+  }
+  if (tid < 8) W.part[0][tid] = W.part[1][tid] = 1e-3;
+  if (tid == 0) W.tau[0] = W.tau[1] = 1.0;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    vn::update(Ar, Ai, n, P, 0, W, warp, lane);
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    vn::matvec(Ar, Ai, n, P, 0, W, warp, lane);
+    __syncthreads();
+  }
+  long long t2 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    if (warp == 0) vn::reflector(Ar, Ai, n, P, 0, W, lane);
+    __syncthreads();
+  }
+  long long t3 = clock64();
+  for (int r = 0; r < reps; ++r) __syncthreads();
+  long long t4 = clock64();
+  if (tid == 0 && blockIdx.x == 0) {
+    clk[0] = (t1 - t0) / reps;
+    clk[1] = (t2 - t1) / reps;
+    clk[2] = (t3 - t2) / reps;
+    clk[3] = (t4 - t3) / reps;
+  }
+}
+
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 64, reps = argc > 2 ? atoi(argv[2]) : 20;
   int sms = 0;
@@ -82,7 +129,7 @@ int main(int argc, char** argv) {
   double* ent;
   cudaMalloc(&clk, 3 * sizeof(long long));
   cudaMalloc(&ent, sizeof(double) * sms * reps);
-  const int bytes = 2 * n * (n + 1) * 8 + sizeof(vn::Scratch) + 2 * n * n * 8;
+  const int bytes = 2 * n * (n + 4) * 8 + sizeof(vn::Scratch) + 2 * n * n * 8;
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   bench<<<sms, 256, bytes>>>(n, 1, clk, ent);  // warm-up
   cudaEvent_t a, b;
@@ -104,5 +151,17 @@ int main(int argc, char** argv) {
   cudaMemcpy(&e0, ent, 8, cudaMemcpyDeviceToHost);
   printf("{\"n\": %d, \"reps\": %d, \"tridiag_clk\": %lld, \"eig_clk\": %lld, \"sum_clk\": %lld, "
          "\"kernel_ms\": %.3f, \"entropy0\": %.17g}\n", n, reps, h[0], h[1], h[2], ms, e0);
+  {
+    long long* c4;
+    cudaMalloc(&c4, 4 * sizeof(long long));
+    const int pb = 2 * n * (n + 4) * 8 + sizeof(vn::Scratch);
+    cudaFuncSetAttribute(pieces, cudaFuncAttributeMaxDynamicSharedMemorySize, pb);
+    pieces<<<sms, 256, pb>>>(n, 50, c4);
+    cudaDeviceSynchronize();
+    long long h4[4];
+    cudaMemcpy(h4, c4, sizeof(h4), cudaMemcpyDeviceToHost);
+    printf("{\"n\": %d, \"update_clk\": %lld, \"matvec_clk\": %lld, \"reflector_clk\": %lld, \"sync_clk\": %lld}\n",
+           n, h4[0], h4[1], h4[2], h4[3]);
+  }
   return 0;
 }
