@@ -15,6 +15,7 @@
 
 #include "hbm_tier.cuh"
 #include "tg_internal.h"
+#include "vn.cuh"
 
 namespace tg {
 namespace hbm {
@@ -28,6 +29,10 @@ struct HHeader {
 };
 constexpr int kHHeaderBytes = (static_cast<int>(sizeof(HHeader)) + 127) / 128 * 128;
 constexpr int kSmemBytes = kHHeaderBytes + kStages * kStage * 8;
+// von Neumann (KIND 1, S = 13: d_a = 64 = one tile, CS = 1): rho planes (pitch 68) and the
+// solver scratch reuse the stage buffers once the GEMM pipeline has drained.
+constexpr int kRP = TB + 4;
+static_assert(2 * TB * kRP * 8 + static_cast<int>(sizeof(vn::Scratch)) <= kStages * kStage * 8, "vN region");
 
 template <int CS>
 __device__ __forceinline__ void sync_all() {
@@ -114,11 +119,26 @@ __device__ void renormalize(const Geo& G, double* X, double* Y, int tid, int war
 
 // TRACE: phase stamps (clock64) of the first cluster's first replica into P.trace[steps][8]:
 // 0 step start, 1 gate pass done, 2 GEMM done, 3 decision done (profiling probe only).
-template <bool TRACE, int CS>
+// KIND: 0 Renyi-2, 1 von Neumann (S = 13, CS = 1; vn.cuh after the GEMM).
+template <bool TRACE, int CS, int KIND>
 __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealParams P) {
+  static_assert(KIND == 0 || CS == 1, "von Neumann runs one CTA per replica");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   HHeader& H = *reinterpret_cast<HHeader*>(smem_raw);
   double* stages = reinterpret_cast<double*>(smem_raw + kHHeaderBytes);
+  double* Rr = stages;  // KIND 1 only (aliases the drained stages)
+  double* Ri = stages + TB * kRP;
+  vn::Scratch& VW = *reinterpret_cast<vn::Scratch*>(stages + 2 * TB * kRP);
+  // entropy of the proposal whose rho the last GEMM produced (valid in thread 0)
+  auto entropy_of = [&](double rho2) -> double {
+    if constexpr (KIND == 0) return smem::renyi2(rho2);
+    return vn::entropy(Rr, Ri, TB, kRP, VW, threadIdx.x, [] { __syncthreads(); });
+  };
+  auto gemm = [&](const double* X, const double* Y, int first, int stride, double out[4]) {
+    const int tid = threadIdx.x;
+    rho_partials<KIND == 1>(Geo(static_cast<int>(P.spins)), X, Y, stages, tid, tid >> 5, tid & 31, first,
+                            stride, P.inject_fault != 0, out, Rr, Ri, kRP);
+  };
   const Geo G(static_cast<int>(P.spins));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = CS == 1 ? 0u : cluster_rank();
@@ -158,12 +178,12 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     if (P.initial_state == 1) renormalize<CS>(G, PX(0), PY(0), tid, warp, lane, rank, H);
 
     double out[4], rho2, tr;
-    rho_partials(G, PX(cur), PY(cur), stages, tid, warp, lane, first, stride, P.inject_fault != 0, out);
+    gemm(PX(cur), PY(cur), first, stride, out);
     if (lane == 0)
       for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
     publish_vals<CS>(H, tid, rank);
     totals<CS>(H, rho2, tr);
-    double cur_e = smem::renyi2(rho2);  // spinmc.cpp:234
+    double cur_e = entropy_of(rho2);  // spinmc.cpp:234 (thread 0)
     bool err = smem::not_normalized(tr);
     if (tid == 0 && writer) {
       P.status[r] = err ? kRowNotNormalized : kRowOk;
@@ -179,13 +199,13 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
       __threadfence();
       sync_all<CS>();
       mark(r, s, 1);
-      rho_partials(G, PX(cur ^ 1), PY(cur ^ 1), stages, tid, warp, lane, first, stride,
-                   P.inject_fault != 0, out);
+      gemm(PX(cur ^ 1), PY(cur ^ 1), first, stride, out);
       if (lane == 0)
         for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
       publish_vals<CS>(H, tid, rank);
-      mark(r, s, 2);
       totals<CS>(H, rho2, tr);
+      const double e_new = entropy_of(rho2);
+      mark(r, s, 2);
       if (tid == 0) {  // every rank decides identically; rank 0 writes
         int acc = 0;
         if (smem::not_normalized(tr)) {
@@ -196,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
           }
         } else {
           H.error = 0;
-          const double proposed = smem::renyi2(rho2);
+          const double proposed = e_new;
           const double delta = P.objective == 0 ? proposed - cur_e : cur_e - proposed;
           acc = g.u < acceptance(delta, g.temp);
           if (acc) cur_e = proposed;
@@ -252,6 +272,7 @@ __global__ void gate_probe_kernel(int spins, const double* psi, int site, const 
   }
 }
 
+template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) entropy_probe_kernel(int spins, const double* psi_all,
                                                                      double* scratch, double* e_out,
                                                                      double* n_out, bool fault) {
@@ -270,14 +291,23 @@ __global__ void __launch_bounds__(kThreads, 1) entropy_probe_kernel(int spins, c
   __threadfence_block();
   __syncthreads();
   double out[4];
-  rho_partials(G, X, Y, stages, tid, warp, lane, 0, 1, fault, out);
+  double* Rr = stages;
+  double* Ri = stages + TB * kRP;
+  rho_partials<KIND == 1>(G, X, Y, stages, tid, warp, lane, 0, 1, fault, out, Rr, Ri, kRP);
   if (lane == 0)
     for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
   publish_vals<1>(H, tid, 0);
+  double rho2, tr;
+  totals<1>(H, rho2, tr);
+  double e = 0.0;
+  if constexpr (KIND == 1) {
+    vn::Scratch& W = *reinterpret_cast<vn::Scratch*>(stages + 2 * TB * kRP);
+    e = vn::entropy(Rr, Ri, TB, kRP, W, tid, [] { __syncthreads(); });
+  } else {
+    e = smem::renyi2(rho2);
+  }
   if (tid == 0) {
-    double rho2, tr;
-    totals<1>(H, rho2, tr);
-    e_out[blockIdx.x] = smem::renyi2(rho2);
+    e_out[blockIdx.x] = e;
     if (n_out) n_out[blockIdx.x] = __dsqrt_rn(tr);
   }
 }
@@ -295,14 +325,16 @@ cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const 
 }
 
 cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* e_out,
-                          double* n_out, bool fault, cudaStream_t s) {
+                          double* n_out, bool fault, cudaStream_t s, bool von_neumann) {
   if (spins < 13 || spins > 24) return cudaErrorInvalidValue;
+  if (von_neumann && spins > static_cast<uint32_t>(kVnMaxSpins)) return cudaErrorInvalidValue;
   double* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, sizeof(double) * 2 * (size_t{1} << spins) * count, s);
   if (e != cudaSuccess) return e;
-  cudaFuncSetAttribute(entropy_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-  entropy_probe_kernel<<<static_cast<unsigned>(count), kThreads, kSmemBytes, s>>>(
-      static_cast<int>(spins), psi, scratch, e_out, n_out, fault);
+  auto k = von_neumann ? entropy_probe_kernel<1> : entropy_probe_kernel<0>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  k<<<static_cast<unsigned>(count), kThreads, kSmemBytes, s>>>(static_cast<int>(spins), psi, scratch, e_out,
+                                                              n_out, fault);
   e = cudaGetLastError();
   cudaFreeAsync(scratch, s);
   return e;
@@ -311,7 +343,8 @@ cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, dou
 // CTAs per replica: 2 when a partial last wave of SMs would otherwise waste >= 2% of the
 // machine (e.g. 512 replicas on 148 SMs: 86.5% -> 98.8%). TG_HBM_CTAS_PER_REPLICA=1|2
 // overrides (tests use it to check both paths agree bitwise).
-int ctas_per_replica(uint64_t rows, int sms) {
+int ctas_per_replica(uint64_t rows, int sms, int entropy_kind) {
+  if (entropy_kind == 0) return 1;  // von Neumann: the eigen-solver runs in one CTA
   if (const char* env = std::getenv("TG_HBM_CTAS_PER_REPLICA")) {
     const int v = std::atoi(env);
     if (v == 1 || v == 2) return v;
@@ -326,10 +359,10 @@ int ctas_per_replica(uint64_t rows, int sms) {
 
 }  // namespace hbm
 
-size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device) {
+size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  const int cs = hbm::ctas_per_replica(rows, sms);
+  const int cs = hbm::ctas_per_replica(rows, sms, entropy_kind);
   const uint64_t clusters = std::min<uint64_t>(rows, static_cast<uint64_t>(sms / cs));
   return static_cast<size_t>(clusters) * 4 * (size_t{1} << spins) * sizeof(double);
 }
@@ -341,14 +374,16 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int cs = hbm::ctas_per_replica(p.rows, sms);
+  const int cs = hbm::ctas_per_replica(p.rows, sms, p.entropy_kind);
+  if (p.entropy_kind == 0 && p.spins > static_cast<uint32_t>(kVnMaxSpins)) return cudaErrorInvalidValue;
   const uint64_t clusters = std::min<uint64_t>(p.rows, static_cast<uint64_t>(sms / cs));
   const int grid = static_cast<int>(clusters) * cs;
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
   void (*kern)(AnnealParams);
-  if (cs == 1) kern = trace ? hbm::anneal_hbm_kernel<true, 1> : hbm::anneal_hbm_kernel<false, 1>;
-  else kern = trace ? hbm::anneal_hbm_kernel<true, 2> : hbm::anneal_hbm_kernel<false, 2>;
+  if (p.entropy_kind == 0) kern = trace ? hbm::anneal_hbm_kernel<true, 1, 1> : hbm::anneal_hbm_kernel<false, 1, 1>;
+  else if (cs == 1) kern = trace ? hbm::anneal_hbm_kernel<true, 1, 0> : hbm::anneal_hbm_kernel<false, 1, 0>;
+  else kern = trace ? hbm::anneal_hbm_kernel<true, 2, 0> : hbm::anneal_hbm_kernel<false, 2, 0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};

@@ -119,8 +119,8 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
 // replica-step + raw draws) stays within this many bytes of workspace.
 constexpr size_t kStreamBudget = size_t{16} << 30;
 
-size_t slab_bytes(uint32_t spins, uint64_t rows, int device) {
-  return spins > static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::anneal_hbm_workspace_bytes(spins, rows, device)
+size_t slab_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind) {
+  return spins > static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::anneal_hbm_workspace_bytes(spins, rows, device, entropy_kind)
                                                          : 0;
 }
 
@@ -128,7 +128,7 @@ size_t slab_bytes(uint32_t spins, uint64_t rows, int device) {
 size_t workspace_for(const tg::AnnealParams& p, int device) {
   const size_t per_row = tg::gate_stream_bytes_per_row(p.spins, p.steps, p.initial_state == 1);
   const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(p.rows, kStreamBudget / per_row));
-  return batch * per_row + slab_bytes(p.spins, batch, device) + 1024;
+  return batch * per_row + slab_bytes(p.spins, batch, device, p.entropy_kind) + 1024;
 }
 
 // Kernels this library has launched (process lifetime): tg_kernel_launches().
@@ -143,7 +143,7 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
   if (p.rows == 0) return cudaSuccess;
   const size_t per_row = tg::gate_stream_bytes_per_row(p.spins, p.steps, p.initial_state == 1);
   uint64_t batch = std::min<uint64_t>(p.rows, kStreamBudget / per_row);
-  while (batch > 0 && batch * per_row + slab_bytes(p.spins, batch, dev) + 1024 > ws_bytes) --batch;
+  while (batch > 0 && batch * per_row + slab_bytes(p.spins, batch, dev, p.entropy_kind) + 1024 > ws_bytes) --batch;
   if (batch == 0) return cudaErrorMemoryAllocation;
   const size_t stream_bytes = batch * per_row;
   char* base = static_cast<char*>(ws);

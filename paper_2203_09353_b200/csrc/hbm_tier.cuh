@@ -111,9 +111,13 @@ __device__ __forceinline__ void load_stage(const double* X, const double* Y, int
 // tile parity: out = {rho2_even, rho2_odd, tr_even, tr_odd}, warp-reduced (all lanes).
 // inject_fault flips the sign of the first accumulation term of rho(0,0) (linalg.cpp:94)
 // after the trace is taken.
+// STORE (von Neumann, single tile d_a = TB only): after the pipeline drains, rho is also
+// written to planar SMEM Rr/Ri (pitch RP), which may alias the (then free) stage buffers.
+template <bool STORE = false>
 __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, const double* Y,
                                              double* stages, int tid, int warp, int lane,
-                                             int first, int stride, bool fault, double out[4]) {
+                                             int first, int stride, bool fault, double out[4],
+                                             double* Rr = nullptr, double* Ri = nullptr, int RP = 0) {
   const int wr = warp / T8::WC, wc = warp % T8::WC;
   const int m = lane >> 2, kq = lane & 3;
   const int nk = G.kchunks(), nt = G.tiles();
@@ -168,20 +172,23 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
         }
     }
     if (it % nk == nk - 1) {  // tile epilogue
-      const int t = first + (it / nk) * stride, ti = t / nt, tj = t % nt, c = t & 1;
+      const int t = first + (it / nk) * stride, ti = t / nt, tj = t % nt;
+      const bool odd = t & 1;  // chain by tile parity (selects, not a dynamic index: no local memory)
       if (ti == tj) {
+        double tsum = odd ? tr[1] : tr[0];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             if (wr * 2 + i == wc * 4 + j) {
-              if (m == 2 * kq) tr[c] += cr[i][j][0];
-              if (m == 2 * kq + 1) tr[c] += cr[i][j][1];
+              if (m == 2 * kq) tsum += cr[i][j][0];
+              if (m == 2 * kq + 1) tsum += cr[i][j][1];
             }
+        if (odd) tr[1] = tsum; else tr[0] = tsum;
       }
       if (fault && t == 0 && wr == 0 && wc == 0 && lane == 0)
         cr[0][0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);
-      double acc = rho[c];
+      double acc = odd ? rho[1] : rho[0];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -190,10 +197,12 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
           for (int e = 0; e < 2; ++e) {
             acc = fma(cr[i][j][e], cr[i][j][e], acc);
             acc = fma(ci[i][j][e], ci[i][j][e], acc);
-            cr[i][j][e] = 0.0;
-            ci[i][j][e] = 0.0;
+            if constexpr (!STORE) {
+              cr[i][j][e] = 0.0;
+              ci[i][j][e] = 0.0;
+            }
           }
-      rho[c] = acc;
+      if (odd) rho[1] = acc; else rho[0] = acc;
     }
   }
   cp_async_wait<0>();
@@ -202,12 +211,25 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
   out[2] = warp_sum(tr[0]);
   out[3] = warp_sum(tr[1]);
   consumer_sync(kThreads);  // all warps done with the stages before they are reused
+  if constexpr (STORE) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int o = (wr * 2 + i) * 8 + m + ((wc * 4 + j) * 8 + 2 * kq + e) * RP;
+          Rr[o] = cr[i][j][e];
+          Ri[o] = ci[i][j][e];
+        }
+    consumer_sync(kThreads);
+  }
 }
 
 cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const double* u,
                              double* out, cudaStream_t s);
 cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* e,
-                          double* n, bool fault, cudaStream_t s);
+                          double* n, bool fault, cudaStream_t s, bool von_neumann = false);
 
 }  // namespace hbm
 }  // namespace tg

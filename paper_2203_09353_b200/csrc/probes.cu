@@ -232,7 +232,7 @@ cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, dou
     case 10: return entropy_s<10>(count, psi, e, n, fault, s, von_neumann);
     case 11: return entropy_s<11>(count, psi, e, n, fault, s, von_neumann);
     case 12: return entropy_s<12>(count, psi, e, n, fault, s, von_neumann);
-    default: return hbm::probe_entropy(spins, count, psi, e, n, fault, s);
+    default: return hbm::probe_entropy(spins, count, psi, e, n, fault, s, von_neumann);
   }
 }
 

@@ -47,7 +47,7 @@ cudaError_t launch_gate_stream(const AnnealParams& p, void* ws, size_t ws_bytes,
 enum : int32_t { kRowOk = 0, kRowNotNormalized = 2 };
 
 constexpr int kSmemMaxSpins = 12;
-constexpr int kVnMaxSpins = 12;  // device von Neumann (vn.cuh): d_a <= 64, SMEM tier
+constexpr int kVnMaxSpins = 13;  // device von Neumann (vn.cuh): d_a <= 64 (SMEM tier, HBM tier S=13)
 
 // anneal_smem.cu (S <= 12)
 cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* grid_out,
@@ -55,7 +55,7 @@ cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* 
 // anneal_hbm.cu (S >= 13)
 cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out,
                               bool trace = false);
-size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device);
+size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind);
 
 // probes.cu
 cudaError_t probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* d_out, cudaStream_t s);

@@ -44,7 +44,7 @@ def load_traj(name):
 
 
 TRAJ_CASES = ["cfg1", "s12", "s14", "s16", "rand_min_s7", "rand_s13", "s5_renorm7", "s2", "s3", "frozen_min_s6"]
-VN_CASES = ["vn_cfg1", "vn_s12", "vn_rand_min_s10", "vn_s3", "vn_s5_renorm7"]  # von Neumann entropy
+VN_CASES = ["vn_cfg1", "vn_s12", "vn_rand_min_s10", "vn_s3", "vn_s5_renorm7", "vn_rand_s13"]  # von Neumann entropy
 
 
 def entropy_kind_of(g) -> int:

@@ -88,7 +88,7 @@ def test_t5_rho_entropy_vs_reference(kats, spins):
     assert np.abs(n - 1.0).max() <= 1e-13
 
 
-@pytest.mark.parametrize("spins", [2, 3, 4, 6, 8, 9, 12])
+@pytest.mark.parametrize("spins", [2, 3, 4, 6, 8, 9, 12, 13])
 def test_t5_von_neumann_vs_reference(kats, oracle, spins):
     """Device eigen-solver (vn.cuh: Householder + Sturm multisection) against the reference's
     cyclic Jacobi (linalg.cpp:161-232) on the golden states (the oracle's bitwise restatement
@@ -102,7 +102,7 @@ def test_t5_von_neumann_vs_reference(kats, oracle, spins):
     assert np.abs(n - 1.0).max() <= 1e-13
 
 
-@pytest.mark.parametrize("spins", [5, 7, 10, 11, 12])
+@pytest.mark.parametrize("spins", [5, 7, 10, 11, 12, 13])
 def test_t5_von_neumann_structured_states(oracle, spins):
     """Spectra the annealer produces: product states (rank 1), low Schmidt rank with
     degenerate and tiny (<1e-15, dropped) eigenvalues, and Haar-random (full rank)."""

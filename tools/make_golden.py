@@ -99,6 +99,7 @@ def trajectories(r, only) -> None:
         "vn_rand_min_s10": (McCfg(spins=10, steps=200, entropy_kind=0, initial_state=1, objective=1), 4),
         "vn_s3": (McCfg(spins=3, steps=200, entropy_kind=0), 4),
         "vn_s5_renorm7": (McCfg(spins=5, steps=150, entropy_kind=0, renormalize_interval=7), 4),
+        "vn_rand_s13": (McCfg(spins=13, steps=60, entropy_kind=0, initial_state=1), 3),  # HBM tier
     }
     for name, (cfg, n) in cases.items():
         if only and name not in only:
