@@ -369,36 +369,101 @@ bool suite_gemm(uint64_t seed, std::string& detail) {  // verify.cpp:33-70
   return worst <= 1e-13;
 }
 
-bool suite_entropy(uint64_t seed, std::string& detail) {  // verify.cpp:72-114 (Renyi-2)
+// Host check values for `verify entropy` (the reference's oracle.cpp:31-44 partial trace,
+// then cyclic Jacobi for the spectrum): independent of the device's rho and eigen-solver.
+std::vector<double> host_spectrum(const std::vector<cplx>& psi, uint32_t spins) {
+  const size_t n = size_t{1} << spins, da = size_t{1} << (spins / 2), db = n / da;
+  std::vector<cplx> w(da * da);
+  for (size_t a1 = 0; a1 < da; ++a1)
+    for (size_t a2 = 0; a2 < da; ++a2) {
+      cplx s = 0.0;
+      for (size_t b = 0; b < db; ++b) s += psi[a1 + b * da] * std::conj(psi[a2 + b * da]);
+      w[a1 + a2 * da] = s;
+    }
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (size_t p = 0; p < da; ++p)
+      for (size_t q = 0; q < da; ++q)
+        if (p != q) off += std::norm(w[p + q * da]);
+    if (off < 1e-30) break;
+    for (size_t p = 0; p + 1 < da; ++p)
+      for (size_t q = p + 1; q < da; ++q) {
+        const cplx b = w[p + q * da];
+        const double ab = std::abs(b);
+        if (ab == 0.0) continue;
+        const cplx ph = b / ab;
+        const double app = w[p + p * da].real(), aqq = w[q + q * da].real();
+        const double tau = (aqq - app) / (2.0 * ab);
+        const double t = (tau >= 0 ? 1.0 : -1.0) / (std::abs(tau) + std::sqrt(1.0 + tau * tau));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = t * c;
+        for (size_t i = 0; i < da; ++i) {  // columns p, q: W G
+          const cplx wp = w[i + p * da], wq = w[i + q * da];
+          w[i + p * da] = c * ph * wp - sn * wq;
+          w[i + q * da] = sn * ph * wp + c * wq;
+        }
+        for (size_t j = 0; j < da; ++j) {  // rows p, q: G^H (W G)
+          const cplx wp = w[p + j * da], wq = w[q + j * da];
+          w[p + j * da] = c * std::conj(ph) * wp - sn * wq;
+          w[q + j * da] = sn * std::conj(ph) * wp + c * wq;
+        }
+      }
+  }
+  std::vector<double> lam(da);
+  for (size_t i = 0; i < da; ++i) lam[i] = w[i + i * da].real();
+  std::sort(lam.begin(), lam.end());
+  return lam;
+}
+
+double device_entropy(const std::vector<cplx>& psi, uint32_t spins, int32_t kind) {
+  double got = 0.0, norm = 0.0;
+  check(tg_probe_entropy_kind(spins, 1, reinterpret_cast<const double*>(psi.data()), kind, &got, &norm));
+  return got;
+}
+
+// verify.cpp:72-114: device von Neumann of random states vs a host partial trace, the
+// product state (0) and GHZ(5) (ln 2, both kinds), on the rho path the anneal kernels use.
+bool suite_entropy(uint64_t seed, std::string& detail) {
   std::mt19937_64 rng(seed);
   std::normal_distribution<double> nd;
   double worst = 0.0;
   for (uint32_t spins : {2u, 4u, 6u, 8u}) {
-    const size_t n = size_t{1} << spins, da = size_t{1} << (spins / 2), db = n / da;
-    std::vector<cplx> psi(n);
-    double nrm = 0.0;
-    for (auto& x : psi) {
-      x = cplx(nd(rng), nd(rng));
-      nrm += std::norm(x);
-    }
-    for (auto& x : psi) x /= std::sqrt(nrm);
-    // host partial trace (oracle.cpp:31-44) and Renyi-2
-    double f2 = 0.0;
-    for (size_t a1 = 0; a1 < da; ++a1)
-      for (size_t a2 = 0; a2 < da; ++a2) {
-        cplx s = 0.0;
-        for (size_t b = 0; b < db; ++b) s += psi[a1 + b * da] * std::conj(psi[a2 + b * da]);
-        f2 += std::norm(s);
+    for (int trial = 0; trial < 8; ++trial) {
+      const size_t n = size_t{1} << spins;
+      std::vector<cplx> psi(n);
+      double nrm = 0.0;
+      for (auto& x : psi) {
+        x = cplx(nd(rng), nd(rng));
+        nrm += std::norm(x);
       }
-    const double want = std::max(-std::log(f2), 0.0);
-    // the device computes it inside the anneal kernel: a 0-step run starting from this state
-    // is not expressible through the ABI, so the probe that shares the kernel's code is used
-    double got = 0.0, norm = 0.0;
-    check(tg_probe_entropy(spins, 1, reinterpret_cast<double*>(psi.data()), &got, &norm));
-    worst = std::max(worst, std::abs(got - want));
+      for (auto& x : psi) x /= std::sqrt(nrm);
+      double want = 0.0;
+      for (double l : host_spectrum(psi, spins))
+        if (l > 1e-15) want -= l * std::log(l);
+      worst = std::max(worst, std::abs(device_entropy(psi, spins, TG_VON_NEUMANN) - std::max(want, 0.0)));
+    }
   }
-  detail = "Renyi-2 of random states S in {2,4,6,8} vs host partial trace, max |diff| " + fmt17(worst);
-  return worst <= 1e-10;
+  if (worst > 1e-9) {
+    detail = "von Neumann entropy deviates from partial-trace oracle by " + fmt17(worst);
+    return false;
+  }
+  std::vector<cplx> prod(64, 0.0);
+  prod[0] = 1.0;
+  const double pe = device_entropy(prod, 6, TG_VON_NEUMANN);
+  if (std::abs(pe) > 1e-10) {
+    detail = "product state entropy " + fmt17(pe) + " (expected 0)";
+    return false;
+  }
+  std::vector<cplx> ghz(32, 0.0);
+  ghz[0] = ghz[31] = 1.0 / std::sqrt(2.0);
+  for (int32_t kind : {TG_VON_NEUMANN, TG_RENYI2}) {
+    const double g = device_entropy(ghz, 5, kind);
+    if (std::abs(g - std::log(2.0)) > 1e-10) {
+      detail = "GHZ entropy " + fmt17(g) + " (expected ln 2)";
+      return false;
+    }
+  }
+  detail = "oracle agreement within " + fmt17(worst);
+  return true;
 }
 
 bool suite_cross(uint64_t seed, std::string& detail) {  // verify.cpp:116-162
@@ -408,7 +473,7 @@ bool suite_cross(uint64_t seed, std::string& detail) {  // verify.cpp:116-162
   c.steps = 40;
   c.procedures = 4;
   c.seed = seed;
-  c.entropy_kind = TG_RENYI2;
+  c.entropy_kind = TG_VON_NEUMANN;  // verify.cpp:126
   c.t0 = 1.0;
   c.t_min = 1e-3;
   c.renormalize_interval = 1000;
@@ -517,7 +582,7 @@ int main(int argc, char** argv) {
         else if (a == "--kernel-log") o.kernel_log = true;
         else if (a == "--help" || a == "-h") {
           std::printf("taskgemm_b200 run [--spins S] [--steps N] [--procedures P] [--devices G] "
-                      "[--mode device] [--entropy renyi-2] [--objective max|min] [--t0 T] "
+                      "[--mode device] [--entropy renyi-2|von-neumann] [--objective max|min] [--t0 T] "
                       "[--t-min T] [--initial-state product|random] [--seed X] "
                       "[--sweep-procedures a,b,..] [--repeats R] [--baseline report.json] "
                       "[--out DIR] [--kernel-log]\n");

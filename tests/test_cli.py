@@ -92,6 +92,25 @@ def test_trace_matches_reference_golden(tmp_path):
 
 
 @gpu
+def test_run_von_neumann_config1(tmp_path):
+    """--entropy von-neumann (the McConfig default kind) on config 1 vs the reference's golden
+    trajectory (second line)."""
+    import numpy as np
+    g = np.load(os.path.join(ROOT, "tests", "golden", "traj_vn_cfg1.npz"))
+    code, out = run(["run", "--spins", "8", "--steps", "1000", "--procedures", "64", "--seed", "0",
+                     "--entropy", "von-neumann", "--out", str(tmp_path)])
+    assert code == 0, out
+    rows = [line.split(",") for line in (tmp_path / "trace.csv").read_text().splitlines()[1:]]
+    acc = np.array([int(r[3]) for r in rows], np.uint8).reshape(64, 1000)
+    assert np.array_equal(acc, g["accepted"])
+    rep = json.loads((tmp_path / "report.json").read_text())
+    assert rep["config"]["entropy"] == "von-neumann"
+    assert abs(rep["average_entropy_nats"] - 2.360208109374111) <= 1e-10 * 2.37
+    code, out = run(["run", "--spins", "14", "--steps", "1", "--entropy", "von-neumann", "--out", str(tmp_path / "x")])
+    assert code != 0 and "device von-neumann entropy covers spins <= 13" in out
+
+
+@gpu
 def test_seed_env_and_flag_precedence(tmp_path):
     env_dir, flag_dir = tmp_path / "env", tmp_path / "flag"
     base = ["run", "--spins", "6", "--steps", "60", "--procedures", "1", "--out"]
