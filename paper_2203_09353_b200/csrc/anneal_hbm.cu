@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     }
 
     int64_t t_prev = (tid == 0 && P.wall_ns) ? globaltimer() : 0;
+    uint64_t renorm_left = P.renorm;  // countdown: no 64-bit modulo per step
     for (uint64_t s = 0; s < P.steps && !err; ++s) {
       const GateRec& g = recs[s];
       mark(r, s, 0);
@@ -238,8 +239,10 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
       __syncthreads();
       err = H.error != 0;
       if (H.decision) cur ^= 1;
-      if (!err && P.renorm > 0 && (s + 1) % P.renorm == 0)
-        renormalize<CS>(G, PX(cur), PY(cur), tid, warp, lane, rank, H);  // spinmc.cpp:246-248
+      if (P.renorm > 0 && --renorm_left == 0) {  // (s + 1) % renorm == 0, spinmc.cpp:246-248
+        renorm_left = P.renorm;
+        if (!err) renormalize<CS>(G, PX(cur), PY(cur), tid, warp, lane, rank, H);
+      }
     }
     if (tid == 0 && writer && P.final_entropy) P.final_entropy[r] = cur_e;
     sync_all<CS>();  // the slab is rewritten by the cluster's next replica

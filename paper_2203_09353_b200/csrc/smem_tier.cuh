@@ -54,7 +54,8 @@ struct Header {  // HBM tier CTA scratch
 constexpr int kHeaderBytes = (static_cast<int>(sizeof(Header)) + 127) / 128 * 128;
 
 // Gate application (spinmc.cpp:91-136) planar SMEM -> planar SMEM, fused form:
-// re = fma(-ui, vi, fma(ur, vr, re)); im = fma(ui, vr, fma(ur, vi, im)), ascending y.
+// re = fma(-ui, vi, fma(ur, vr, re)); im = fma(ui, vr, fma(ur, vi, im)) over the four inputs
+// (in a lane-rotated order, below).
 // Same sum as the reference (re += ur*vr - ui*vi) with fused rounding: 64 DFMA per group
 // instead of 128 DMUL/DADD. On sm_100a DMMA and DFMA share the FP64 pipe, so the gate's
 // op count is paid directly out of the GEMM's budget; the result differs from the
@@ -64,24 +65,37 @@ __device__ __forceinline__ void gate_pass_fma(const double* __restrict__ sx,
                                               const double* __restrict__ sy,
                                               double* __restrict__ dx, double* __restrict__ dy,
                                               int site, const R& g, int tid, int nthreads) {
+  // Bank-conflict-free order: for site <= 3 the 16 groups of a half-warp share few residues
+  // mod 16 (site 0: bases 4*gi -> 4 banks, 4-way conflicts). Each lane walks its group's
+  // four amplitudes in an order rotated by a lane constant r (r = (tid>>2)&3, or (tid>>3)&1
+  // at site 3), which makes the 16 addresses of every load/store distinct mod 16. U is
+  // permuted once (rows and columns by r), so the inner loop has no dynamic register index.
+  // (nthreads is a multiple of 16, so r only depends on tid.)
+  const int r = site <= 2 ? (tid >> 2) & 3 : (site == 3 ? (tid >> 3) & 1 : 0);
   double ur[16], ui[16];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    ur[e] = g.ur[e];
-    ui[e] = g.ui[e];
-  }
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int e = ((a + r) & 3) * 4 + ((b + r) & 3);
+      ur[a * 4 + b] = g.ur[e];
+      ui[a * 4 + b] = g.ui[e];
+    }
   constexpr int GROUPS = D::N / 4;
   const int lo_mask = (1 << site) - 1;
-#pragma unroll 2
+  int off[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) off[t] = ((t + r) & 3) << site;
+#pragma unroll 4
   for (int gi = tid; gi < GROUPS; gi += nthreads) {
     const int base = ((gi >> site) << (site + 2)) | (gi & lo_mask);
     int ph[4];
     double vr[4], vi[4];
 #pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      ph[y] = D::phys(base | (y << site));
-      vr[y] = sx[ph[y]];
-      vi[y] = sy[ph[y]];
+    for (int t = 0; t < 4; ++t) {
+      ph[t] = D::phys(base | off[t]);
+      vr[t] = sx[ph[t]];
+      vi[t] = sy[ph[t]];
     }
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
@@ -155,20 +169,23 @@ __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
         }
     if (fault && wr == 0 && wc == 0 && lane == 0)
       cr[0][0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);
+    double part[4] = {0.0, 0.0, 0.0, 0.0};  // four chains: the fold is not one 32-deep DFMA chain
 #pragma unroll
     for (int i = 0; i < T::TM; ++i)
 #pragma unroll
       for (int j = 0; j < T::TN; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          rho2 = fma(cr[i][j][e], cr[i][j][e], rho2);
-          rho2 = fma(ci[i][j][e], ci[i][j][e], rho2);
+          double& a = part[((i * T::TN + j) * 2 + e) & 3];
+          a = fma(cr[i][j][e], cr[i][j][e], a);
+          a = fma(ci[i][j][e], ci[i][j][e], a);
           if constexpr (STORE) {
             const int o = (wr * T::TM + i) * 8 + m + ((wc * T::TN + j) * 8 + 2 * kq + e) * RP;
             Rr[o] = cr[i][j][e];
             Ri[o] = ci[i][j][e];
           }
         }
+    rho2 = (part[0] + part[1]) + (part[2] + part[3]);
   }
   rho2 = warp_sum(rho2);
   trace = warp_sum(trace);
