@@ -53,7 +53,7 @@ __global__ void apply_gate_smem_kernel(const double* psi, int site, const double
     g.ui[tid] = u[2 * (x + 4 * y) + 1];
   }
   load_state<D>(psi, planes, planes + D::PLANE, tid, blockDim.x);
-  smem::gate_pass_fma<D>(planes, planes + D::PLANE, planes + 2 * D::PLANE, planes + 3 * D::PLANE,
+  smem::gate_pass<D>(planes, planes + D::PLANE, planes + 2 * D::PLANE, planes + 3 * D::PLANE,
                      site, g, tid, blockDim.x);
   __syncthreads();
   for (int idx = tid; idx < D::N; idx += blockDim.x) {

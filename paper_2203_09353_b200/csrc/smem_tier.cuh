@@ -2,16 +2,16 @@
 // psi' live in shared memory for the whole trajectory (HBM traffic per step ~ 0).
 //
 // Layout: each buffer is two planes (X = Re, Y = Im) of a column-major d_a x d_b
-// matrix Psi[a][b] = psi[a + b*d_a] (spinmc.cpp:145-148), stored with pitch
-// PITCH = DA_PAD + 4 doubles per column b. 2*PITCH == 8 or 24 (mod 32) words, so the
-// DMMA fragment pattern (8 consecutive a x 4 consecutive b per warp) is bank-conflict
-// free. Rows >= d_a and columns >= d_b (S < 6) are zero padding.
-//
-// rho = Psi Psi^dagger by real split:
-//   Re rho = X X^T + Y Y^T,  Im rho = Y X^T - X Y^T,
-// four DMMA.8x8x4 per 8x8 complex block and k-chunk of 4 (2048 flop = 8*8*8*4). rho
-// never leaves registers: the epilogue reduces sum |rho_ij|^2 (Renyi-2) and trace(rho)
-// (= ||psi'||^2, the norm check of spinmc.cpp:152-156) per warp, fixed order.
+// matrix Psi[a][b] = psi[a + b*d_a] (spinmc.cpp:145-148).
+//  * d_a >= 16 (S >= 8): dense column pitch d_a with an XOR swizzle of row bits 2-3,
+//      phys(a, b) = b*d_a + (a ^ 4*((f(b) ^ (a >> 4)) & 3)),  f(b) = (b ^ b>>2 ^ b>>4) & 3.
+//    phys is GF(2)-linear in the amplitude index (phys(i ^ j) = phys(i) ^ phys(j)), so an
+//    address is one XOR of a per-lane constant and a per-chunk value. It keeps the GEMM
+//    fragments (8 consecutive a x 4 consecutive b) and the DMMA gate's fragments
+//    (tools/swizzle_check.py) bank-conflict free at every site, and needs no padding:
+//    the S=12 buffers are 64 KB.
+//  * d_a <= 8: pitch DA_PAD + 4 doubles (2*PITCH == 8 or 24 mod 32 words); rows >= d_a and
+//    columns >= d_b are zero padding.
 #pragma once
 #include "tg_device.cuh"
 
@@ -24,15 +24,27 @@ constexpr int kConsumers = kConsumerWarps * 32;
 template <int LA, int LB>
 struct Dims {
   static constexpr int DA = 1 << LA, DB = 1 << LB;
+  static constexpr bool SWZ = LA >= 4;  // swizzled dense layout (else padded)
   static constexpr int DA_PAD = DA < 8 ? 8 : DA;
   static constexpr int DB_PAD = DB < 4 ? 4 : DB;
-  static constexpr int PITCH = DA_PAD + 4;
+  static constexpr int PITCH = SWZ ? DA : DA_PAD + 4;
   static constexpr int PLANE = DB_PAD * PITCH;  // doubles per plane
   static constexpr int N = 1 << (LA + LB);
   static constexpr int NB = DA_PAD / 8;  // 8x8 blocks per rho dimension
   static constexpr int S = LA + LB;
-  __device__ static __forceinline__ int phys(int idx) {
-    return (idx & (DA - 1)) + (idx >> LA) * PITCH;
+  // Physical offset of amplitude idx (linear over GF(2) when SWZ).
+  __host__ __device__ static constexpr int phys(int idx) {
+    if constexpr (SWZ) {
+      const int b = idx >> LA, a = idx & (DA - 1);
+      return idx ^ ((((b ^ (b >> 2) ^ (b >> 4)) ^ (a >> 4)) & 3) << 2);
+    } else {
+      return (idx & (DA - 1)) + (idx >> LA) * PITCH;
+    }
+  }
+  // Offset of Psi[a][b] (a < DA_PAD, b < DB_PAD; the padding rows/columns only when !SWZ).
+  __host__ __device__ static constexpr int at(int a, int b) {
+    if constexpr (SWZ) return phys(a | (b << LA));
+    else return a + b * PITCH;
   }
 };
 
@@ -111,19 +123,162 @@ __device__ __forceinline__ void gate_pass_fma(const double* __restrict__ sx,
   }
 }
 
+// Gate application in DMMA form (swizzled layout, S >= 8). The gate is the real 8x8 matrix
+// [[Ur, -Ui], [Ui, Ur]] applied to 8 groups at a time: per chunk of 8 groups, two
+// DMMA.8x8x4 (B = the groups' Re / Im amplitudes, k = amplitude y; D rows m < 4 = Re of
+// output x = m, m >= 4 = Im of x = m - 4; D columns = groups). 2 LDS + 2 DMMA + 2 STS per
+// lane per chunk instead of 8 LDS + 64 DFMA + 8 STS per group: the FP64 pipe cost is the
+// same 64 FMA per group, at tensor-pipe issue cost. Same sum as the reference
+// (re = sum_y ur*vr - ui*vi) with the tensor unit's rounding (within a few ulp, §4).
+// Chunk c holds groups 8c + P(n), P a permutation of 0..7 chosen so that loads (lanes
+// 0-15: columns 0-3) and stores (columns 0,2,4,6 / 1,3,5,7) are conflict free; with phys
+// and the group -> amplitude deposit both linear, every address is cb ^ lane constant.
+__device__ __forceinline__ int deposit(int g, int site) {  // spinmc.cpp:118-121 base index
+  return ((g >> site) << (site + 2)) | (g & ((1 << site) - 1));
+}
+// Per-lane constants of the DMMA gate for one record: the A fragments and the lane's
+// load / store offsets (relative to a chunk's base, combined by XOR).
+struct GateLane {
+  double a1, a2;
+  int kload, kst0, kst1, site;
+  bool re;  // this lane's D row is a real part (stores go to the X plane)
+};
+template <class D, class R>
+__device__ __forceinline__ GateLane gate_lane(const R& g, int site, int lane) {
+  GateLane L;
+  const int ml = lane >> 2, kl = lane & 3, x = ml & 3;
+  L.a1 = ml < 4 ? g.ur[x * 4 + kl] : g.ui[x * 4 + kl];
+  L.a2 = ml < 4 ? -g.ui[x * 4 + kl] : g.ur[x * 4 + kl];
+  auto P = [site](int n) { return site == 0 ? n : ((n & 4) | ((n ^ (n >> 2)) & 3)); };
+  L.kload = D::phys(deposit(P(ml), site) | (kl << site));
+  L.kst0 = D::phys(deposit(P(2 * kl), site) | (x << site));
+  L.kst1 = D::phys(deposit(P(2 * kl + 1), site) | (x << site));
+  L.site = site;
+  L.re = ml < 4;
+  return L;
+}
+// One chunk (8 groups, c = chunk index): 2 LDS + 2 DMMA + 2 STS per lane.
+template <class D>
+__device__ __forceinline__ void gate_chunk(const GateLane& L, const double* __restrict__ sx,
+                                           const double* __restrict__ sy, double* __restrict__ dst,
+                                           int c) {
+  const int cb = D::phys(deposit(8 * c, L.site));
+  const double vr = sx[cb ^ L.kload], vi = sy[cb ^ L.kload];
+  double d0 = 0.0, d1 = 0.0;
+  dmma(d0, d1, L.a1, vr);
+  dmma(d0, d1, L.a2, vi);
+  dst[cb ^ L.kst0] = d0;
+  dst[cb ^ L.kst1] = d1;
+}
+template <class D, class R>
+__device__ __forceinline__ void gate_pass_dmma(const double* __restrict__ sx,
+                                               const double* __restrict__ sy,
+                                               double* __restrict__ dx, double* __restrict__ dy,
+                                               int site, const R& g, int warp, int lane) {
+  static_assert(D::SWZ && D::N >= 256, "DMMA gate needs the swizzled layout");
+  const GateLane L = gate_lane<D>(g, site, lane);
+  double* __restrict__ dst = L.re ? dx : dy;
+  // A warp takes chunks warp, warp + 8, ... in batches of B: all loads of a batch, then its
+  // 2B DMMAs (B independent chains), then its stores — the loads of a batch never wait
+  // behind stores that might alias, and the DMMA latency (26 clk) overlaps across chunks.
+  constexpr int CH = D::N / 32;
+  constexpr int PER = CH / kConsumerWarps;  // chunks per warp (>= 1 for S >= 8)
+  constexpr int B = PER < 4 ? PER : 4;
+#pragma unroll 1
+  for (int c0 = warp; c0 < CH; c0 += kConsumerWarps * B) {
+    int cb[B];
+    double vr[B], vi[B], d0[B], d1[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      cb[b] = D::phys(deposit(8 * (c0 + b * kConsumerWarps), L.site));
+      vr[b] = sx[cb[b] ^ L.kload];
+      vi[b] = sy[cb[b] ^ L.kload];
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      d0[b] = 0.0;
+      d1[b] = 0.0;
+      dmma(d0[b], d1[b], L.a1, vr[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) dmma(d0[b], d1[b], L.a2, vi[b]);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      dst[cb[b] ^ L.kst0] = d0[b];
+      dst[cb[b] ^ L.kst1] = d1[b];
+    }
+  }
+}
+
+// The tier's gate: DMMA form on the swizzled layout, fused DFMA form otherwise.
+template <class D, class R>
+__device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const double* __restrict__ sy,
+                                          double* __restrict__ dx, double* __restrict__ dy, int site,
+                                          const R& g, int tid, int nthreads) {
+  if constexpr (D::SWZ) gate_pass_dmma<D>(sx, sy, dx, dy, site, g, tid >> 5, tid & 31);
+  else gate_pass_fma<D>(sx, sy, dx, dy, site, g, tid, nthreads);
+}
+
 // Per-warp sum |rho_ij|^2 and trace(rho) of rho = Psi Psi^dagger (warp-reduced; valid in
 // every lane). inject_fault flips the sign of the first accumulation term of rho(0,0)
 // (linalg.cpp:94 testhook) AFTER the trace is taken, so only the entropy is corrupted.
 // STORE (von Neumann): rho is also written to planar SMEM Rr/Ri (column-major, pitch RP).
-template <class D, bool STORE = false>
+// SPEC (swizzled layout; a compile-time switch so the gate stages schedule freely with the
+// GEMM's loads and DMMAs): the warps also apply the NEXT step's gate to this Psi (the
+// speculative proposal for "accepted", written to gdst = X or Y plane of a third buffer by
+// lane), one 8-group chunk interleaved after every RATIO-th k-step of the GEMM, so its
+// DMMAs and SMEM traffic share the GEMM's pipeline instead of a separate phase. It is the
+// same DMMA computation as gate_pass_dmma: bitwise the non-speculative proposal.
+template <class D, bool STORE = false, bool SPEC = false>
 __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
                                              const double* __restrict__ Y, int warp, int lane,
                                              bool fault, double& rho2, double& trace,
                                              double* Rr = nullptr, double* Ri = nullptr,
-                                             int RP = 0) {
+                                             int RP = 0, const GateLane* SL = nullptr,
+                                             double* __restrict__ gdst = nullptr) {
   using T = Tile<D::NB>;
   rho2 = 0.0;
   trace = 0.0;
+  constexpr int GPW = D::N / 32 / kConsumerWarps;        // gate chunks per warp
+  constexpr int KI = D::DB_PAD / 4;                      // GEMM k-steps
+  constexpr int RATIO = GPW > 0 && KI >= GPW ? KI / GPW : 1;
+  static_assert(!SPEC || (D::SWZ && GPW >= 1 && KI % GPW == 0), "speculative gate layout");
+  if (SPEC && warp >= T::WR * T::WC) {  // warps without a GEMM tile (S < 10)
+#pragma unroll 1
+    for (int i = 0; i < GPW; ++i) gate_chunk<D>(*SL, X, Y, gdst, warp + kConsumerWarps * i);
+  }
+  // Speculative gate, software-pipelined over the k-steps: chunk j is loaded at k-step
+  // j*RATIO, its two DMMAs issue one and two k-steps later and it is stored three k-steps
+  // later; a stage runs at the top of its k-step, ahead of the GEMM's loads and DMMAs, so
+  // no instruction waits on a gate result (DMMA latency 26 clk) and the warp's GEMM issue
+  // never stalls behind the gate.
+  int g_cb = 0, h_cb = 0, r_cb = 0;
+  double g_vr = 0.0, g_vi = 0.0, h_vi = 0.0, h_d0 = 0.0, h_d1 = 0.0, r_d0 = 0.0, r_d1 = 0.0;
+  auto at_chunk = [&](int it, int lag) { return it >= lag && (it - lag) % RATIO == 0 && (it - lag) / RATIO < GPW; };
+  auto spec_stage = [&](int it) {
+    if (at_chunk(it, 3)) {  // store chunk (it-3)/RATIO
+      gdst[r_cb ^ SL->kst0] = r_d0;
+      gdst[r_cb ^ SL->kst1] = r_d1;
+    }
+    if (at_chunk(it, 2)) {  // second DMMA (Im inputs)
+      dmma(h_d0, h_d1, SL->a2, h_vi);
+      r_d0 = h_d0;
+      r_d1 = h_d1;
+      r_cb = h_cb;
+    }
+    if (at_chunk(it, 1)) {  // first DMMA (Re inputs)
+      h_d0 = 0.0;
+      h_d1 = 0.0;
+      dmma(h_d0, h_d1, SL->a1, g_vr);
+      h_vi = g_vi;
+      h_cb = g_cb;
+    }
+    if (at_chunk(it, 0)) {  // loads
+      g_cb = D::phys(deposit(8 * (warp + kConsumerWarps * (it / RATIO)), SL->site));
+      g_vr = X[g_cb ^ SL->kload];
+      g_vi = Y[g_cb ^ SL->kload];
+    }
+  };
   if (warp < T::WR * T::WC) {
     const int wr = warp / T::WC, wc = warp % T::WC;
     const int m = lane >> 2, kq = lane & 3;
@@ -132,22 +287,35 @@ __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
     for (int i = 0; i < T::TM; ++i)
 #pragma unroll
       for (int j = 0; j < T::TN; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    // Fragment offsets: at(row, kb + kq) = kb * PITCH + ro[f(kb)] with f(kb) in 0..3 (the
+    // swizzle term of column kb + kq, kb a multiple of 4), so each load is a per-lane base
+    // register plus an immediate.
+    constexpr int NV = D::SWZ ? 4 : 1;
+    int roa[T::TM][NV], rob[T::TN][NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int c = D::SWZ ? 4 * v : 0;  // a column with f(c) = v
+#pragma unroll
+      for (int i = 0; i < T::TM; ++i) roa[i][v] = D::at((wr * T::TM + i) * 8 + m, kq + c) - c * D::PITCH;
+#pragma unroll
+      for (int j = 0; j < T::TN; ++j) rob[j][v] = D::at((wc * T::TN + j) * 8 + m, kq + c) - c * D::PITCH;
+    }
 #pragma unroll
     for (int kb = 0; kb < D::DB_PAD; kb += 4) {
-      const int col = (kb + kq) * D::PITCH;
+      if constexpr (SPEC) spec_stage(kb / 4);
+      const int v = D::SWZ ? (((kb >> 2) ^ (kb >> 4)) & 3) : 0;
+      const int ko = kb * D::PITCH;
       double xa[T::TM], ya[T::TM], xn[T::TM], xb[T::TN], yb[T::TN];
 #pragma unroll
       for (int i = 0; i < T::TM; ++i) {
-        const int row = (wr * T::TM + i) * 8 + m;
-        xa[i] = X[row + col];
-        ya[i] = Y[row + col];
+        xa[i] = X[roa[i][v] + ko];
+        ya[i] = Y[roa[i][v] + ko];
         xn[i] = -xa[i];
       }
 #pragma unroll
       for (int j = 0; j < T::TN; ++j) {
-        const int row = (wc * T::TN + j) * 8 + m;
-        xb[j] = X[row + col];
-        yb[j] = Y[row + col];
+        xb[j] = X[rob[j][v] + ko];
+        yb[j] = Y[rob[j][v] + ko];
       }
 #pragma unroll
       for (int i = 0; i < T::TM; ++i)
@@ -158,6 +326,11 @@ __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
           dmma(ci[i][j][0], ci[i][j][1], ya[i], xb[j]);
           dmma(ci[i][j][0], ci[i][j][1], xn[i], yb[j]);
         }
+    }
+    if constexpr (SPEC) {
+      spec_stage(KI);
+      spec_stage(KI + 1);
+      spec_stage(KI + 2);
     }
 #pragma unroll
     for (int i = 0; i < T::TM; ++i)
