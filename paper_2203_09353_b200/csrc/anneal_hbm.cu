@@ -134,10 +134,11 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     if constexpr (KIND == 0) return smem::renyi2(rho2);
     return vn::entropy(Rr, Ri, TB, kRP, VW, threadIdx.x, [] { __syncthreads(); });
   };
+  int64_t* gprof = nullptr;  // TRACE: GEMM-internal clocks of the current step (slots 4..6)
   auto gemm = [&](const double* X, const double* Y, int first, int stride, double out[4]) {
     const int tid = threadIdx.x;
     rho_partials<KIND == 1>(Geo(static_cast<int>(P.spins)), X, Y, stages, tid, tid >> 5, tid & 31, first,
-                            stride, P.inject_fault != 0, out, Rr, Ri, kRP);
+                            stride, P.inject_fault != 0, out, Rr, Ri, kRP, gprof);
   };
   const Geo G(static_cast<int>(P.spins));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -200,7 +201,9 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
       __threadfence();
       sync_all<CS>();
       mark(r, s, 1);
+      if (TRACE && rank == 0 && r == 0 && s < P.steps) gprof = P.trace + s * 8 + 4;
       gemm(PX(cur ^ 1), PY(cur ^ 1), first, stride, out);
+      gprof = nullptr;
       if (lane == 0)
         for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
       publish_vals<CS>(H, tid, rank);

@@ -55,6 +55,24 @@ __device__ __forceinline__ void st_cluster_f64(double* local, uint32_t rank, dou
 
 // Gate application (spinmc.cpp:91-136) on groups [g0, g1), global planar -> global planar,
 // reference rounding (bitwise the reference's psi' for the same U). R: GateRec.
+// A thread takes a pair of groups {2q, 2q+1}: for site >= 1 their four amplitude pairs are
+// adjacent (base(2q+1) = base(2q) + 1), for site 0 the pair is 8 consecutive amplitudes, so
+// every access is a 16-byte ld/st.cg and a thread has 16 loads in flight before it
+// computes (the pass is HBM/L2 latency bound, not FP64 bound).
+__device__ __forceinline__ void gate_apply(const double* ur, const double* ui, const double vr[4],
+                                           const double vi[4], double re_out[4], double im_out[4]) {
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    double re = 0.0, im = 0.0;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      re = __dadd_rn(re, __dsub_rn(__dmul_rn(ur[x * 4 + y], vr[y]), __dmul_rn(ui[x * 4 + y], vi[y])));
+      im = __dadd_rn(im, __dadd_rn(__dmul_rn(ur[x * 4 + y], vi[y]), __dmul_rn(ui[x * 4 + y], vr[y])));
+    }
+    re_out[x] = re;
+    im_out[x] = im;
+  }
+}
 template <class R>
 __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const double* __restrict__ sy,
                                           double* __restrict__ dx, double* __restrict__ dy,
@@ -67,24 +85,48 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const d
     ui[e] = g.ui[e];
   }
   const int lo_mask = (1 << site) - 1;
-  for (int gi = g0 + tid; gi < g1; gi += nthreads) {
+  for (int q = (g0 >> 1) + tid; q < (g1 >> 1); q += nthreads) {
+    const int gi = 2 * q;
     const int base = ((gi >> site) << (site + 2)) | (gi & lo_mask);
-    double vr[4], vi[4];
+    double2 lr[4], li[4];  // site >= 1: amplitude y of groups (2q, 2q+1); site 0: 8 consecutive
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
-      vr[y] = __ldcg(sx + (base | (y << site)));
-      vi[y] = __ldcg(sy + (base | (y << site)));
+      const int o = site == 0 ? base + 2 * y : base + (y << site);
+      lr[y] = __ldcg(reinterpret_cast<const double2*>(sx + o));
+      li[y] = __ldcg(reinterpret_cast<const double2*>(sy + o));
     }
+    double vr[2][4], vi[2][4];
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      if (site == 0) {  // group 2q: amplitudes base..base+3, group 2q+1: base+4..base+7
+        const double2 a = lr[y], b = li[y];
+        vr[y >> 1][2 * (y & 1)] = a.x;
+        vr[y >> 1][2 * (y & 1) + 1] = a.y;
+        vi[y >> 1][2 * (y & 1)] = b.x;
+        vi[y >> 1][2 * (y & 1) + 1] = b.y;
+      } else {
+        vr[0][y] = lr[y].x;
+        vr[1][y] = lr[y].y;
+        vi[0][y] = li[y].x;
+        vi[1][y] = li[y].y;
+      }
+    }
+    double ro[2][4], io[2][4];
+    gate_apply(ur, ui, vr[0], vi[0], ro[0], io[0]);
+    gate_apply(ur, ui, vr[1], vi[1], ro[1], io[1]);
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
-      double re = 0.0, im = 0.0;
-#pragma unroll
-      for (int y = 0; y < 4; ++y) {
-        re = __dadd_rn(re, __dsub_rn(__dmul_rn(ur[x * 4 + y], vr[y]), __dmul_rn(ui[x * 4 + y], vi[y])));
-        im = __dadd_rn(im, __dadd_rn(__dmul_rn(ur[x * 4 + y], vi[y]), __dmul_rn(ui[x * 4 + y], vr[y])));
+      double2 a, b;
+      if (site == 0) {
+        a = make_double2(ro[x >> 1][2 * (x & 1)], ro[x >> 1][2 * (x & 1) + 1]);
+        b = make_double2(io[x >> 1][2 * (x & 1)], io[x >> 1][2 * (x & 1) + 1]);
+      } else {
+        a = make_double2(ro[0][x], ro[1][x]);
+        b = make_double2(io[0][x], io[1][x]);
       }
-      __stcg(dx + (base | (x << site)), re);
-      __stcg(dy + (base | (x << site)), im);
+      const int o = site == 0 ? base + 2 * x : base + (x << site);
+      __stcg(reinterpret_cast<double2*>(dx + o), a);
+      __stcg(reinterpret_cast<double2*>(dy + o), b);
     }
   }
 }
@@ -94,15 +136,14 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const d
 // thread tid copies row-pair rp = tid & 31 of columns 8*(i & 3) + (tid >> 5), plane-panel
 // i >> 2 (i = 0..15), so all index math is per-thread constants plus one chunk offset.
 __device__ __forceinline__ void load_stage(const double* X, const double* Y, int da, int ti, int tj,
-                                           int kc, double* stage, int tid) {
+                                           int kc, double* stage, int tid, int i0 = 0, int i1 = 16) {
   const int rp = tid & 31, c0 = tid >> 5;
-  const double* srcA = nullptr;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
+  for (int i = i0; i < i1; ++i) {
     const int pp = i >> 2, col = 8 * (i & 3) + c0;
-    srcA = (pp & 1) ? Y : X;
+    const double* src = (pp & 1) ? Y : X;
     const int row0 = ((pp >> 1) ? tj : ti) * TB;
-    const double* g = srcA + (row0 + 2 * rp) + static_cast<size_t>(kc * KC + col) * da;
+    const double* g = src + (row0 + 2 * rp) + static_cast<size_t>(kc * KC + col) * da;
     cp_async16(stage + pp * kPanel + col * SP + 2 * rp, g);
   }
 }
@@ -117,18 +158,24 @@ template <bool STORE = false>
 __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, const double* Y,
                                              double* stages, int tid, int warp, int lane,
                                              int first, int stride, bool fault, double out[4],
-                                             double* Rr = nullptr, double* Ri = nullptr, int RP = 0) {
+                                             double* Rr = nullptr, double* Ri = nullptr, int RP = 0,
+                                             int64_t* prof = nullptr) {
+  // prof (profiling probe only, thread 0): [0] clk in the chunk waits + barriers,
+  // [1] clk in tile epilogues, [2] clk until the first chunk landed.
+  int64_t t_wait = 0, t_epi = 0, t_first = 0;
+  const int64_t t_start = prof ? clock64() : 0;
   const int wr = warp / T8::WC, wc = warp % T8::WC;
   const int m = lane >> 2, kq = lane & 3;
   const int nk = G.kchunks(), nt = G.tiles();
   const int mine = (nt * nt - first + stride - 1) / stride;
+  const int lnt = G.la - 6, lnk = (G.spins - G.la) - 5;  // log2 of nt = d_a/64, nk = d_b/32
   const int total = mine * nk;
   double cr[2][4][2], ci[2][4][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-  double rho[2] = {0.0, 0.0}, tr[2] = {0.0, 0.0};
+  double rho[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}}, tr[2] = {0.0, 0.0};
   auto issue = [&](int it) {
     if (it < total) {
       const int t = first + (it / nk) * stride, kc = it % nk;
@@ -139,13 +186,46 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
   issue(0);
   issue(1);
   for (int it = 0; it < total; ++it) {
+    const int64_t tw0 = prof ? clock64() : 0;
     cp_async_wait<1>();       // this thread's copies of stage `it` landed
     consumer_sync(kThreads);  // everyone's did; stage (it-1) % 3 is free
-    issue(it + 2);
+    if (prof) {
+      const int64_t tw1 = clock64();
+      t_wait += tw1 - tw0;
+      if (it == 0) t_first = tw1 - t_start;
+    }
+    // stage it+2 is issued 2 copies per k-step, spread over the chunk's 8 k-steps (keeps
+    // the LSU queue short). Its addresses are set up here, once per chunk, as 32-bit
+    // offsets from X (Y = X + n): an address computation inside the k-steps sits on the
+    // warps' issue path right after their DMMAs and, with both warps of an SMSP in step
+    // after the barrier, leaves the DMMA pipe idle (measured: ~15% of the GEMM).
+    const int nx = it + 2;
+    const bool has_next = nx < total;
+    uint32_t soff[4];
+    uint32_t doff;
+    {
+      const int tn = first + (nx >> lnk) * stride, kcn = nx & (nk - 1);
+      const int ti = tn >> lnt, tj = tn & (nt - 1);
+      const int rp = tid & 31, c0 = tid >> 5;
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp)
+        soff[pp] = static_cast<uint32_t>((pp & 1) * G.n + ((pp >> 1) ? tj : ti) * TB + 2 * rp) +
+                   static_cast<uint32_t>(kcn * KC + c0) * static_cast<uint32_t>(G.da);
+      doff = static_cast<uint32_t>((nx % kStages) * kStage + c0 * SP + 2 * rp);
+    }
+    const uint32_t col8 = 8u * static_cast<uint32_t>(G.da);
     const double* st = stages + (it % kStages) * kStage;
     const double *AX = st, *AY = st + kPanel, *BX = st + 2 * kPanel, *BY = st + 3 * kPanel;
 #pragma unroll
     for (int kb = 0; kb < KC; kb += 4) {
+      if (has_next) {
+#pragma unroll
+        for (int i = kb / 2; i < kb / 2 + 2; ++i) {  // copy i: panel-plane i >> 2, column 8 * (i & 3) + c0
+          const int pp = i >> 2, j = i & 3;
+          cp_async16(stages + doff + pp * kPanel + 8 * j * SP, X + (soff[pp] + j * col8));
+        }
+      }
+      if (kb == KC - 4) cp_async_commit();
       const int col = (kb + kq) * SP;
       double xa[2], ya[2], xn[2], xb[4], yb[4];
 #pragma unroll
@@ -172,6 +252,7 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
         }
     }
     if (it % nk == nk - 1) {  // tile epilogue
+      const int64_t te0 = prof ? clock64() : 0;
       const int t = first + (it / nk) * stride, ti = t / nt, tj = t % nt;
       const bool odd = t & 1;  // chain by tile parity (selects, not a dynamic index: no local memory)
       if (ti == tj) {
@@ -188,26 +269,47 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
       }
       if (fault && t == 0 && wr == 0 && wc == 0 && lane == 0)
         cr[0][0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);
-      double acc = odd ? rho[1] : rho[0];
+      // four interleaved chains per parity: the fold is 8 DFMA deep instead of 32 (it runs
+      // next to other warps' DMMA streams, which starve FP64 latency chains)
+      double acc[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = odd ? rho[1][c] : rho[0][c];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            acc = fma(cr[i][j][e], cr[i][j][e], acc);
-            acc = fma(ci[i][j][e], ci[i][j][e], acc);
+            double& a = acc[((i * 4 + j) * 2 + e) & 3];
+            a = fma(cr[i][j][e], cr[i][j][e], a);
+            a = fma(ci[i][j][e], ci[i][j][e], a);
             if constexpr (!STORE) {
               cr[i][j][e] = 0.0;
               ci[i][j][e] = 0.0;
             }
           }
-      if (odd) rho[1] = acc; else rho[0] = acc;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (odd) rho[1][c] = acc[c]; else rho[0][c] = acc[c];
+      }
+      if (prof) t_epi += clock64() - te0;
+    }
+  }
+  if (prof) {  // [2]: the largest per-warp wait (thread 0's is [0])
+    __shared__ int64_t wwait[kWarps];
+    if (lane == 0) wwait[warp] = t_wait;
+    consumer_sync(kThreads);
+    if (tid == 0) {
+      int64_t mx = 0;
+      for (int w = 0; w < kWarps; ++w) mx = wwait[w] > mx ? wwait[w] : mx;
+      prof[0] = t_wait;
+      prof[1] = t_epi;
+      prof[2] = mx + 0 * t_first;
     }
   }
   cp_async_wait<0>();
-  out[0] = warp_sum(rho[0]);
-  out[1] = warp_sum(rho[1]);
+  out[0] = warp_sum((rho[0][0] + rho[0][1]) + (rho[0][2] + rho[0][3]));
+  out[1] = warp_sum((rho[1][0] + rho[1][1]) + (rho[1][2] + rho[1][3]));
   out[2] = warp_sum(tr[0]);
   out[3] = warp_sum(tr[1]);
   consumer_sync(kThreads);  // all warps done with the stages before they are reused

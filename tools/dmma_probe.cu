@@ -37,11 +37,21 @@ __global__ void chains(int iters, long long* cyc, double* sink) {
 
 // GEMM-tile pattern: SMEM panel 4 planes x 32 cols x 68 pitch (like hbm_tier.cuh), warp
 // grid 4x2 of 16x32 sub-tiles (TM=2, TN=4) — only the first 8 warps' roles, repeated.
-template <int PIPE>
+template <int PIPE, bool RANDOM = false>
 __global__ void tile(int iters, long long* cyc, double* sink) {
   extern __shared__ double sm[];
   constexpr int SP = 68, KP = 32 * SP;
-  for (int i = threadIdx.x; i < 6 * KP; i += blockDim.x) sm[i] = 1.0 + i * 1e-12;
+  for (int i = threadIdx.x; i < 6 * KP; i += blockDim.x) {
+    if (RANDOM) {  // state-like data: random signs/mantissas, magnitudes ~2^-6 (|psi| ~ 1/64)
+      unsigned long long z = (i + 1) * 0x9E3779B97F4A7C15ull;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      z ^= z >> 31;
+      sm[i] = (static_cast<double>(z >> 11) * 0x1.0p-53 - 0.5) * 0.03;
+    } else {
+      sm[i] = 1.0 + i * 1e-12;
+    }
+  }
   double* gout = sm + 4 * KP;  // PIPE 2: gate-chunk stores (another buffer)
   double g_vr = 0, g_vi = 0, r0 = 0, r1 = 0;
   const double ga1 = 0.5 + threadIdx.x * 1e-6, ga2 = 0.25 - threadIdx.x * 1e-6;
@@ -84,6 +94,16 @@ __global__ void tile(int iters, long long* cyc, double* sink) {
             dmma(ci[i][j][0], ci[i][j][1], ya[i], xb[j]);
           }
         }
+      if (PIPE == 5) {  // + 2 cp.async (16 B, L2-resident global) per k4 per thread, like the HBM tier
+        const double* g = sink + 64 + ((blockIdx.x * 8192 + it * 512 + kb * 64 + threadIdx.x * 2) & ((1 << 21) - 1));
+        double* d = gout + ((threadIdx.x * 2 + kb * 128) & 2047);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(d)), "l"(g) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(d + 512)), "l"(g + 512) : "memory");
+        if (kb == 28) {
+          asm volatile("cp.async.commit_group;\n" ::: "memory");
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        }
+      }
       if (PIPE == 3) {  // gate-chunk DMMAs only (no SMEM traffic)
         r0 = 0; r1 = 0;
         dmma(r0, r1, ga1, g_vr);
@@ -137,7 +157,8 @@ double run(K kern, int warps, int iters, int dmma_per_warp_iter, int smem) {
   long long* cyc;
   double* sink;
   cudaMalloc(&cyc, sms * sizeof(long long));
-  cudaMalloc(&sink, 64);
+  cudaMalloc(&sink, (64 + (1 << 21) + 4096) * sizeof(double));
+  cudaMemset(sink, 0, (64 + (1 << 21) + 4096) * sizeof(double));
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   kern<<<sms, warps * 32, smem>>>(iters / 4, cyc, sink);
   kern<<<sms, warps * 32, smem>>>(iters, cyc, sink);
@@ -169,5 +190,9 @@ int main() {
     printf("tile W=%2d: adjacent pairs %.3f  split pairs %.3f  +gate chunk %.3f  +gate DMMA only %.3f  +gate SMEM only %.3f DMMA/clk/SM\n", w,
            run(tile<0>, w, 500, 256, smem), run(tile<1>, w, 500, 256, smem), run(tile<2>, w, 500, 272, smem),
            run(tile<3>, w, 500, 272, smem), run(tile<4>, w, 500, 256, smem));
+  for (int w : Wt) printf("tile W=%2d: + 2 cp.async/k4/thread %.3f DMMA/clk/SM\n", w, run(tile<5>, w, 500, 256, smem));
+  for (int w : Wt)
+    printf("tile W=%2d, random state-like data: adjacent pairs %.3f  (1.0-ish data %.3f) DMMA/clk/SM\n", w,
+           run(tile<0, true>, w, 500, 256, smem), run(tile<0, false>, w, 500, 256, smem));
   return 0;
 }

@@ -27,6 +27,12 @@ rows = {
     "decision (thread 0)": s[:, 3] - s[:, 2],
     "decision -> next step start": nxt[:, 0] - s[:, 3],
 }
+if spins >= 13:  # HBM tier: GEMM-internal clocks (thread 0)
+    rows.update({
+        "  GEMM: chunk waits + barriers": s[:, 4],
+        "  GEMM: tile epilogues": s[:, 5],
+        "  GEMM: max per-warp chunk waits": s[:, 6],
+    })
 print(f"S={spins} replicas={replicas} steps={steps}")
 for k, v in rows.items():
     print(f"  {k:32s} median {np.median(v):8.0f} clk   mean {np.mean(v):8.0f}")
