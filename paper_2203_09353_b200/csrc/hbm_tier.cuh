@@ -85,25 +85,41 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const d
     ui[e] = g.ui[e];
   }
   const int lo_mask = (1 << site) - 1;
-  for (int q = (g0 >> 1) + tid; q < (g1 >> 1); q += nthreads) {
+  auto offset = [&](int q, int y) {  // amplitude offset of load/store y of pair q
     const int gi = 2 * q;
     const int base = ((gi >> site) << (site + 2)) | (gi & lo_mask);
-    double2 lr[4], li[4];  // site >= 1: amplitude y of groups (2q, 2q+1); site 0: 8 consecutive
+    return site == 0 ? base + 2 * y : base + (y << site);
+  };
+  // software-pipelined: the loads of the thread's next pair are issued before the current
+  // pair is computed and stored (stores would otherwise fence the next loads: one L2/HBM
+  // round trip per pair)
+  double2 lr[4], li[4], nr[4], ni[4];
+  const int q1 = g1 >> 1;
+  int q = (g0 >> 1) + tid;
+  if (q < q1) {
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
-      const int o = site == 0 ? base + 2 * y : base + (y << site);
-      lr[y] = __ldcg(reinterpret_cast<const double2*>(sx + o));
-      li[y] = __ldcg(reinterpret_cast<const double2*>(sy + o));
+      lr[y] = __ldcg(reinterpret_cast<const double2*>(sx + offset(q, y)));
+      li[y] = __ldcg(reinterpret_cast<const double2*>(sy + offset(q, y)));
+    }
+  }
+  for (; q < q1; q += nthreads) {
+    const int qn = q + nthreads;
+    if (qn < q1) {
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        nr[y] = __ldcg(reinterpret_cast<const double2*>(sx + offset(qn, y)));
+        ni[y] = __ldcg(reinterpret_cast<const double2*>(sy + offset(qn, y)));
+      }
     }
     double vr[2][4], vi[2][4];
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
       if (site == 0) {  // group 2q: amplitudes base..base+3, group 2q+1: base+4..base+7
-        const double2 a = lr[y], b = li[y];
-        vr[y >> 1][2 * (y & 1)] = a.x;
-        vr[y >> 1][2 * (y & 1) + 1] = a.y;
-        vi[y >> 1][2 * (y & 1)] = b.x;
-        vi[y >> 1][2 * (y & 1) + 1] = b.y;
+        vr[y >> 1][2 * (y & 1)] = lr[y].x;
+        vr[y >> 1][2 * (y & 1) + 1] = lr[y].y;
+        vi[y >> 1][2 * (y & 1)] = li[y].x;
+        vi[y >> 1][2 * (y & 1) + 1] = li[y].y;
       } else {
         vr[0][y] = lr[y].x;
         vr[1][y] = lr[y].y;
@@ -124,9 +140,13 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const d
         a = make_double2(ro[0][x], ro[1][x]);
         b = make_double2(io[0][x], io[1][x]);
       }
-      const int o = site == 0 ? base + 2 * x : base + (x << site);
-      __stcg(reinterpret_cast<double2*>(dx + o), a);
-      __stcg(reinterpret_cast<double2*>(dy + o), b);
+      __stcg(reinterpret_cast<double2*>(dx + offset(q, x)), a);
+      __stcg(reinterpret_cast<double2*>(dy + offset(q, x)), b);
+    }
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      lr[y] = nr[y];
+      li[y] = ni[y];
     }
   }
 }

@@ -142,6 +142,10 @@ struct GateLane {
   double a1, a2;
   int kload, kst0, kst1, site;
   bool re;  // this lane's D row is a real part (stores go to the X plane)
+  // speculative gate (rho_partials SPEC): chunk warp + 8i has base cbw ^ tab[i]
+  // (phys and the deposit are linear), tab = the CTA's table for this site
+  int cbw;
+  const int* tab;
 };
 template <class D, class R>
 __device__ __forceinline__ GateLane gate_lane(const R& g, int site, int lane) {
@@ -274,7 +278,7 @@ __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
       h_cb = g_cb;
     }
     if (at_chunk(it, 0)) {  // loads
-      g_cb = D::phys(deposit(8 * (warp + kConsumerWarps * (it / RATIO)), SL->site));
+      g_cb = SL->cbw ^ SL->tab[it / RATIO];
       g_vr = X[g_cb ^ SL->kload];
       g_vi = Y[g_cb ^ SL->kload];
     }
