@@ -16,6 +16,7 @@
 #include "hbm_tier.cuh"
 #include "tg_internal.h"
 #include "vn.cuh"
+#include "vn_packed.cuh"
 
 namespace tg {
 namespace hbm {
@@ -33,6 +34,11 @@ constexpr int kSmemBytes = kHHeaderBytes + kStages * kStage * 8;
 // solver scratch reuse the stage buffers once the GEMM pipeline has drained.
 constexpr int kRP = TB + 4;
 static_assert(2 * TB * kRP * 8 + static_cast<int>(sizeof(vn::Scratch)) <= kStages * kStage * 8, "vN region");
+// von Neumann at S = 14, 15 (d_a = 128): packed lower Hermitian part + solver scratch in the
+// drained stages (vn_packed.cuh); rho itself goes through the slab's extra planes.
+constexpr int kPackedN = vnp::kMaxN;
+constexpr int kPackedPlane = (vnp::packed_size(kPackedN) + 15) / 16 * 16;
+static_assert(2 * kPackedPlane * 8 + static_cast<int>(sizeof(vnp::Scratch)) <= kStages * kStage * 8, "vN packed region");
 
 template <int CS>
 __device__ __forceinline__ void sync_all() {
@@ -129,22 +135,42 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   double* Rr = stages;  // KIND 1 only (aliases the drained stages)
   double* Ri = stages + TB * kRP;
   vn::Scratch& VW = *reinterpret_cast<vn::Scratch*>(stages + 2 * TB * kRP);
+  const Geo G0(static_cast<int>(P.spins));
+  const bool packed = KIND == 1 && G0.da > TB;
+  double* Rg = nullptr;  // packed: global rho of the cluster (after its slab)
+  if (packed) Rg = P.workspace + static_cast<size_t>(blockIdx.x) * (4 * static_cast<size_t>(G0.n) +
+                                                                    2 * static_cast<size_t>(G0.da) * G0.da) +
+                   4 * static_cast<size_t>(G0.n);
   // entropy of the proposal whose rho the last GEMM produced (valid in thread 0)
   auto entropy_of = [&](double rho2) -> double {
-    if constexpr (KIND == 0) return smem::renyi2(rho2);
-    return vn::entropy(Rr, Ri, TB, kRP, VW, threadIdx.x, [] { __syncthreads(); });
+    if constexpr (KIND == 0) {
+      return smem::renyi2(rho2);
+    } else {
+      if (packed) {
+        double* Ar = stages;
+        double* Ai = stages + kPackedPlane;
+        vnp::Scratch& PW = *reinterpret_cast<vnp::Scratch*>(stages + 2 * kPackedPlane);
+        __threadfence_block();
+        __syncthreads();  // every tile of rho is in Rg
+        vnp::build(Rg, Rg + static_cast<size_t>(G0.da) * G0.da, Ar, Ai, G0.da, threadIdx.x);
+        __syncthreads();
+        return vnp::entropy(Ar, Ai, G0.da, PW, threadIdx.x, [] { __syncthreads(); });
+      }
+      return vn::entropy(Rr, Ri, TB, kRP, VW, threadIdx.x, [] { __syncthreads(); });
+    }
   };
   int64_t* gprof = nullptr;  // TRACE: GEMM-internal clocks of the current step (slots 4..6)
   auto gemm = [&](const double* X, const double* Y, int first, int stride, double out[4]) {
     const int tid = threadIdx.x;
     rho_partials<KIND == 1>(Geo(static_cast<int>(P.spins)), X, Y, stages, tid, tid >> 5, tid & 31, first,
-                            stride, P.inject_fault != 0, out, Rr, Ri, kRP, gprof);
+                            stride, P.inject_fault != 0, out, Rr, Ri, kRP, gprof, Rg);
   };
   const Geo G(static_cast<int>(P.spins));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = CS == 1 ? 0u : cluster_rank();
   const uint64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
-  double* slab = P.workspace + static_cast<size_t>(cid) * 4 * G.n;
+  double* slab = P.workspace + static_cast<size_t>(cid) * (4 * static_cast<size_t>(G.n) +
+                                                         (packed ? 2 * static_cast<size_t>(G.da) * G.da : 0));
   auto PX = [&](int b) { return slab + (2 * b) * static_cast<size_t>(G.n); };
   auto PY = [&](int b) { return slab + (2 * b + 1) * static_cast<size_t>(G.n); };
   auto mark = [&](uint64_t r, uint64_t s, int k) {
@@ -299,7 +325,9 @@ __global__ void __launch_bounds__(kThreads, 1) entropy_probe_kernel(int spins, c
   double out[4];
   double* Rr = stages;
   double* Ri = stages + TB * kRP;
-  rho_partials<KIND == 1>(G, X, Y, stages, tid, warp, lane, 0, 1, fault, out, Rr, Ri, kRP);
+  const bool packed = KIND == 1 && G.da > TB;
+  double* Rg = packed ? scratch + 2ull * G.n * gridDim.x + 2ull * G.da * G.da * blockIdx.x : nullptr;
+  rho_partials<KIND == 1>(G, X, Y, stages, tid, warp, lane, 0, 1, fault, out, Rr, Ri, kRP, nullptr, Rg);
   if (lane == 0)
     for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
   publish_vals<1>(H, tid, 0);
@@ -307,8 +335,19 @@ __global__ void __launch_bounds__(kThreads, 1) entropy_probe_kernel(int spins, c
   totals<1>(H, rho2, tr);
   double e = 0.0;
   if constexpr (KIND == 1) {
-    vn::Scratch& W = *reinterpret_cast<vn::Scratch*>(stages + 2 * TB * kRP);
-    e = vn::entropy(Rr, Ri, TB, kRP, W, tid, [] { __syncthreads(); });
+    if (packed) {
+      double* Ar = stages;
+      double* Ai = stages + kPackedPlane;
+      vnp::Scratch& PW = *reinterpret_cast<vnp::Scratch*>(stages + 2 * kPackedPlane);
+      __threadfence_block();
+      __syncthreads();
+      vnp::build(Rg, Rg + static_cast<size_t>(G.da) * G.da, Ar, Ai, G.da, tid);
+      __syncthreads();
+      e = vnp::entropy(Ar, Ai, G.da, PW, tid, [] { __syncthreads(); });
+    } else {
+      vn::Scratch& W = *reinterpret_cast<vn::Scratch*>(stages + 2 * TB * kRP);
+      e = vn::entropy(Rr, Ri, TB, kRP, W, tid, [] { __syncthreads(); });
+    }
   } else {
     e = smem::renyi2(rho2);
   }
@@ -335,7 +374,9 @@ cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, dou
   if (spins < 13 || spins > 24) return cudaErrorInvalidValue;
   if (von_neumann && spins > static_cast<uint32_t>(kVnMaxSpins)) return cudaErrorInvalidValue;
   double* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(&scratch, sizeof(double) * 2 * (size_t{1} << spins) * count, s);
+  const size_t da = size_t{1} << (spins / 2);
+  const size_t per = 2 * (size_t{1} << spins) + (von_neumann && da > TB ? 2 * da * da : 0);
+  cudaError_t e = cudaMallocAsync(&scratch, sizeof(double) * per * count, s);
   if (e != cudaSuccess) return e;
   auto k = von_neumann ? entropy_probe_kernel<1> : entropy_probe_kernel<0>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
@@ -370,7 +411,10 @@ size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const int cs = hbm::ctas_per_replica(rows, sms, entropy_kind);
   const uint64_t clusters = std::min<uint64_t>(rows, static_cast<uint64_t>(sms / cs));
-  return static_cast<size_t>(clusters) * 4 * (size_t{1} << spins) * sizeof(double);
+  const size_t da = size_t{1} << (spins / 2);
+  // von Neumann with d_a > 64: rho (2 planes of d_a^2) after each slab (vn_packed.cuh)
+  const size_t rho = entropy_kind == 0 && da > static_cast<size_t>(hbm::TB) ? 2 * da * da : 0;
+  return static_cast<size_t>(clusters) * (4 * (size_t{1} << spins) + rho) * sizeof(double);
 }
 
 cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out,

@@ -179,7 +179,9 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
                                              double* stages, int tid, int warp, int lane,
                                              int first, int stride, bool fault, double out[4],
                                              double* Rr = nullptr, double* Ri = nullptr, int RP = 0,
-                                             int64_t* prof = nullptr) {
+                                             int64_t* prof = nullptr, double* Rg = nullptr) {
+  // STORE with Rg (von Neumann, d_a > TB): every finished tile is written to the global
+  // column-major planes Rg (Re) and Rg + d_a^2 (Im) instead of SMEM.
   // prof (profiling probe only, thread 0): [0] clk in the chunk waits + barriers,
   // [1] clk in tile epilogues, [2] clk until the first chunk landed.
   int64_t t_wait = 0, t_epi = 0, t_first = 0;
@@ -291,6 +293,20 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
         cr[0][0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);
       // four interleaved chains per parity: the fold is 8 DFMA deep instead of 32 (it runs
       // next to other warps' DMMA streams, which starve FP64 latency chains)
+      if (STORE && Rg) {
+        const size_t pl = static_cast<size_t>(G.da) * G.da;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const size_t o = static_cast<size_t>(ti * TB + (wr * 2 + i) * 8 + m) +
+                               static_cast<size_t>(tj * TB + (wc * 4 + j) * 8 + 2 * kq + e) * G.da;
+              __stcg(Rg + o, cr[i][j][e]);
+              __stcg(Rg + pl + o, ci[i][j][e]);
+            }
+      }
       double acc[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[c] = odd ? rho[1][c] : rho[0][c];
@@ -303,7 +319,7 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
             double& a = acc[((i * 4 + j) * 2 + e) & 3];
             a = fma(cr[i][j][e], cr[i][j][e], a);
             a = fma(ci[i][j][e], ci[i][j][e], a);
-            if constexpr (!STORE) {
+            if (!STORE || Rg) {
               cr[i][j][e] = 0.0;
               ci[i][j][e] = 0.0;
             }
@@ -333,7 +349,7 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
   out[2] = warp_sum(tr[0]);
   out[3] = warp_sum(tr[1]);
   consumer_sync(kThreads);  // all warps done with the stages before they are reused
-  if constexpr (STORE) {
+  if (STORE && !Rg) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll

@@ -47,7 +47,7 @@ cudaError_t launch_gate_stream(const AnnealParams& p, void* ws, size_t ws_bytes,
 enum : int32_t { kRowOk = 0, kRowNotNormalized = 2 };
 
 constexpr int kSmemMaxSpins = 12;
-constexpr int kVnMaxSpins = 13;  // device von Neumann (vn.cuh): d_a <= 64 (SMEM tier, HBM tier S=13)
+constexpr int kVnMaxSpins = 15;  // device von Neumann: d_a <= 64 (vn.cuh: SMEM tier, HBM tier S=13), d_a = 128 (vn_packed.cuh: S=14,15)
 
 // anneal_smem.cu (S <= 12)
 cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* grid_out,

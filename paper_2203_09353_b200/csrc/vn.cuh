@@ -283,7 +283,8 @@ struct Minors {
   }
 };
 
-__device__ __forceinline__ void sturm2(const Scratch& W, int n, double x0, double x1, int& c0, int& c1) {
+template <class SW>  // vn::Scratch or vnp::Scratch
+__device__ __forceinline__ void sturm2(const SW& W, int n, double x0, double x1, int& c0, int& c1) {
   Minors a, b;
   a.init(W.d[0], x0);
   b.init(W.d[0], x1);
@@ -309,8 +310,8 @@ __device__ __forceinline__ void sturm2(const Scratch& W, int n, double x0, doubl
 
 // Step 3: W.lam[0..n) ascending, by multisection: G = 256/n threads per eigenvalue, two
 // points each per round, the bracket shrinks by 2G+1 per round down to ~1 ulp of ||T||.
-template <class Sync>
-__device__ void eigenvalues(int n, Scratch& W, int tid, Sync sync) {
+template <class SW, class Sync>
+__device__ void eigenvalues(int n, SW& W, int tid, Sync sync) {
   const int lane = tid & 31;
   if (tid < 32) {  // Gershgorin bracket (LAPACK dstebz convention)
     double lo = 1e300, hi = -1e300;

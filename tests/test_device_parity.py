@@ -88,9 +88,10 @@ def test_t5_rho_entropy_vs_reference(kats, spins):
     assert np.abs(n - 1.0).max() <= 1e-13
 
 
-@pytest.mark.parametrize("spins", [2, 3, 4, 6, 8, 9, 12, 13])
+@pytest.mark.parametrize("spins", [2, 3, 4, 6, 8, 9, 12, 13, 14])
 def test_t5_von_neumann_vs_reference(kats, oracle, spins):
-    """Device eigen-solver (vn.cuh: Householder + Sturm multisection) against the reference's
+    """Device eigen-solver (vn.cuh, and vn_packed.cuh for d_a = 128: Householder + Sturm
+    multisection) against the reference's
     cyclic Jacobi (linalg.cpp:161-232) on the golden states (the oracle's bitwise restatement
     where the fixture has no vN values)."""
     states = kats[f"ent_{spins}_states"]
@@ -102,7 +103,7 @@ def test_t5_von_neumann_vs_reference(kats, oracle, spins):
     assert np.abs(n - 1.0).max() <= 1e-13
 
 
-@pytest.mark.parametrize("spins", [5, 7, 10, 11, 12, 13])
+@pytest.mark.parametrize("spins", [5, 7, 10, 11, 12, 13, 14, 15])
 def test_t5_von_neumann_structured_states(oracle, spins):
     """Spectra the annealer produces: product states (rank 1), low Schmidt rank with
     degenerate and tiny (<1e-15, dropped) eigenvalues, and Haar-random (full rank)."""
@@ -218,6 +219,21 @@ def test_t7_von_neumann_trajectory_parity(device, name):
     rep = device.run(cfg_from(g))
     assert_traj_parity(rep, g)
     assert abs(rep.average_entropy - float(g["average"])) <= TOL * max(1.0, abs(float(g["average"])))
+
+
+@pytest.mark.parametrize("spins,objective", [(14, "max"), (15, "min")])
+def test_t7_von_neumann_packed_vs_oracle(device, oracle, spins, objective):
+    """d_a = 128 (S = 14, 15): rho through the slab's scratch planes, packed-lower Householder
+    (vn_packed.cuh) inside the anneal loop, against the oracle's Jacobi trajectories."""
+    cfg = tg.ExperimentConfig(spins=spins, steps=6, procedures=2, seed=5, objective=objective,
+                              entropy_kind="von-neumann")
+    rep = device.run(cfg)
+    want = oracle.run(McCfg(spins=spins, steps=6, seed=5, entropy_kind=0,
+                            objective=0 if objective == "max" else 1), 0, 2)
+    assert np.array_equal(rep.sites, want.sites)
+    assert np.array_equal(rep.accepted, want.accepted)
+    assert close(rep.entropies, want.entropies).all(), np.max(np.abs(rep.entropies - want.entropies))
+    assert close(rep.initial_entropy, want.initial).all()
 
 
 def test_t7_von_neumann_appendix_a(device):
