@@ -1,11 +1,12 @@
 // anneal_hbm.cu — persistent annealing kernel, HBM/L2-resident tier (13 <= S <= 24).
 //
-// A cluster of CS CTAs (1 or 2, see hbm_tier.cuh) owns one replica at a time; its psi /
+// A cluster of CS CTAs (1, 2 or 4, see hbm_tier.cuh) owns one replica at a time; its psi /
 // psi' slabs live in the workspace. Per step (metropolis_step, spinmc.cpp:193-213):
-//   gate pass  — rank k applies U to its half of the groups (reference rounding), global
+//   gate pass  — rank k applies U to its 1/CS of the groups (reference rounding), global
 //                -> global; cluster barrier;
-//   GEMM       — rho tiles of the rank's parity on DMMA, fused ||rho||_F^2 and trace;
-//                per-rank chain values exchanged through DSMEM; cluster barrier;
+//   GEMM       — rho tiles t = k (mod CS) on DMMA, fused ||rho||_F^2 and trace in four
+//                canonical chains; per-rank chain values exchanged through DSMEM; cluster
+//                barrier;
 //   decision   — thread 0 of every rank evaluates the same reference formula on the same
 //                totals (identical results); rank 0 writes the trace.
 // Every FP64 op outside the GEMM runs while no DMMA is in flight on the SM (the FP64 pipe
@@ -21,10 +22,11 @@
 namespace tg {
 namespace hbm {
 
+constexpr int kMaxCS = 4;
 struct HHeader {
-  double part[kWarps][4];  // per-warp chain values {rho even, rho odd, tr even, tr odd}
-  double val[2][4];        // per-rank totals (rank 1's arrive by DSMEM)
-  double norm_half[2];
+  double part[kWarps][2 * kChains];  // per-warp chain values {rho chain 0..3, tr chain 0..3}
+  double val[kMaxCS][2 * kChains];   // per-rank chain sums (other ranks' arrive by DSMEM)
+  double norm_q[4];                  // renormalisation: sums over the four quarters of psi
   int32_t decision;
   int32_t error;
 };
@@ -53,49 +55,35 @@ __device__ __forceinline__ void sync_all() {
 template <int CS>
 __device__ __forceinline__ void publish_vals(HHeader& H, int tid, uint32_t rank) {
   __syncthreads();  // per-warp parts written
-  if (tid == 0) {
-    double v[4];
+  if (tid < 2 * kChains) {
+    double v = 0.0;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      v[c] = 0.0;
+    for (int w = 0; w < kWarps; ++w) v += H.part[w][tid];
+    H.val[rank][tid] = v;
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) v[c] += H.part[w][c];
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if constexpr (CS == 1) {
-        H.val[0][c] = v[c];
-      } else {
-        H.val[rank][c] = v[c];
-        st_cluster_f64(&H.val[rank][c], rank ^ 1u, v[c]);
-      }
-    }
+    for (uint32_t d = 1; d < static_cast<uint32_t>(CS); ++d) st_cluster_f64(&H.val[rank][tid], (rank + d) % CS, v);
   }
   sync_all<CS>();
 }
 
-// Totals in the canonical order: even-tile chain + odd-tile chain.
+// Totals in the canonical order ((c0 + c1) + (c2 + c3)); chain c was summed by rank c % CS.
 template <int CS>
 __device__ __forceinline__ void totals(const HHeader& H, double& rho2, double& tr) {
-  if constexpr (CS == 1) {
-    rho2 = H.val[0][0] + H.val[0][1];
-    tr = H.val[0][2] + H.val[0][3];
-  } else {
-    rho2 = H.val[0][0] + H.val[1][1];
-    tr = H.val[0][2] + H.val[1][3];
-  }
+  auto v = [&](int k) { return H.val[(k % kChains) % CS][k]; };
+  rho2 = (v(0) + v(1)) + (v(2) + v(3));
+  tr = (v(4) + v(5)) + (v(6) + v(7));
 }
 
-// renormalize (spinmc.cpp:56-59) over the two halves of psi (rank k owns half k); the
-// total is half0 + half1 whatever CS is, so CS=1 and CS=2 agree bitwise.
+// renormalize (spinmc.cpp:56-59) over the four quarters of psi (rank k owns quarters
+// q = k mod CS); the total is ((q0 + q1) + (q2 + q3)) whatever CS is, so every CS agrees
+// bitwise.
 template <int CS>
 __device__ void renormalize(const Geo& G, double* X, double* Y, int tid, int warp, int lane,
                             uint32_t rank, HHeader& H) {
-  const int half = G.n / 2;
-  for (int h = 0; h < 2; ++h) {
-    if (CS == 2 && h != static_cast<int>(rank)) continue;
+  const int quarter = G.n / 4;
+  for (int q = static_cast<int>(rank); q < 4; q += CS) {
     double s = 0.0;
-    for (int i = h * half + tid; i < (h + 1) * half; i += kThreads) {
+    for (int i = q * quarter + tid; i < (q + 1) * quarter; i += kThreads) {
       const double x = __ldcg(X + i), y = __ldcg(Y + i);
       s = fma(x, x, s);
       s = fma(y, y, s);
@@ -107,14 +95,14 @@ __device__ void renormalize(const Geo& G, double* X, double* Y, int tid, int war
       double t = 0.0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) t += H.part[w][0];
-      H.norm_half[h] = t;
-      if (CS == 2) st_cluster_f64(&H.norm_half[h], rank ^ 1u, t);
+      H.norm_q[q] = t;
+      for (uint32_t d = 1; d < static_cast<uint32_t>(CS); ++d) st_cluster_f64(&H.norm_q[q], (rank + d) % CS, t);
     }
     __syncthreads();
   }
   sync_all<CS>();
-  const double inv = __ddiv_rn(1.0, __dsqrt_rn(H.norm_half[0] + H.norm_half[1]));
-  const int i0 = CS == 2 ? static_cast<int>(rank) * half : 0, i1 = CS == 2 ? i0 + half : G.n;
+  const double inv = __ddiv_rn(1.0, __dsqrt_rn((H.norm_q[0] + H.norm_q[1]) + (H.norm_q[2] + H.norm_q[3])));
+  const int part = G.n / CS, i0 = static_cast<int>(rank) * part, i1 = i0 + part;
   for (int i = i0 + tid; i < i1; i += kThreads) {
     __stcg(X + i, __dmul_rn(__ldcg(X + i), inv));
     __stcg(Y + i, __dmul_rn(__ldcg(Y + i), inv));
@@ -177,15 +165,14 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     if (TRACE && tid == 0 && rank == 0 && r == 0 && s < P.steps) P.trace[s * 8 + k] = clock64();
   };
   const int groups = G.n / 4;
-  const int g0 = CS == 2 ? static_cast<int>(rank) * (groups / 2) : 0;
-  const int g1 = CS == 2 ? g0 + groups / 2 : groups;
+  const int g0 = static_cast<int>(rank) * (groups / CS), g1 = g0 + groups / CS;
   const int first = static_cast<int>(rank), stride = CS;
   const bool writer = rank == 0;
 
   for (uint64_t r = cid; r < P.rows; r += ncl) {
     const GateRec* recs = P.gates + r * P.steps;
     {  // initial state, split by halves of the amplitude index
-      const int i0 = CS == 2 ? static_cast<int>(rank) * (G.n / 2) : 0, i1 = CS == 2 ? i0 + G.n / 2 : G.n;
+      const int i0 = static_cast<int>(rank) * (G.n / CS), i1 = i0 + G.n / CS;
       if (P.initial_state == 0) {
         for (int i = i0 + tid; i < i1; i += kThreads) {  // product_state (spinmc.cpp:28-35)
           __stcg(PX(0) + i, i == 0 ? 1.0 : 0.0);
@@ -204,10 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     int cur = 0;
     if (P.initial_state == 1) renormalize<CS>(G, PX(0), PY(0), tid, warp, lane, rank, H);
 
-    double out[4], rho2, tr;
+    double out[2 * kChains], rho2, tr;
     gemm(PX(cur), PY(cur), first, stride, out);
     if (lane == 0)
-      for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
+      for (int c = 0; c < 2 * kChains; ++c) H.part[warp][c] = out[c];
     publish_vals<CS>(H, tid, rank);
     totals<CS>(H, rho2, tr);
     double cur_e = entropy_of(rho2);  // spinmc.cpp:234 (thread 0)
@@ -231,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
       gemm(PX(cur ^ 1), PY(cur ^ 1), first, stride, out);
       gprof = nullptr;
       if (lane == 0)
-        for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
+        for (int c = 0; c < 2 * kChains; ++c) H.part[warp][c] = out[c];
       publish_vals<CS>(H, tid, rank);
       totals<CS>(H, rho2, tr);
       const double e_new = entropy_of(rho2);
@@ -322,14 +309,14 @@ __global__ void __launch_bounds__(kThreads, 1) entropy_probe_kernel(int spins, c
   }
   __threadfence_block();
   __syncthreads();
-  double out[4];
+  double out[2 * kChains];
   double* Rr = stages;
   double* Ri = stages + TB * kRP;
   const bool packed = KIND == 1 && G.da > TB;
   double* Rg = packed ? scratch + 2ull * G.n * gridDim.x + 2ull * G.da * G.da * blockIdx.x : nullptr;
   rho_partials<KIND == 1>(G, X, Y, stages, tid, warp, lane, 0, 1, fault, out, Rr, Ri, kRP, nullptr, Rg);
   if (lane == 0)
-    for (int c = 0; c < 4; ++c) H.part[warp][c] = out[c];
+    for (int c = 0; c < 2 * kChains; ++c) H.part[warp][c] = out[c];
   publish_vals<1>(H, tid, 0);
   double rho2, tr;
   totals<1>(H, rho2, tr);
@@ -387,21 +374,26 @@ cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, dou
   return e;
 }
 
-// CTAs per replica: 2 when a partial last wave of SMs would otherwise waste >= 2% of the
-// machine (e.g. 512 replicas on 148 SMs: 86.5% -> 98.8%). TG_HBM_CTAS_PER_REPLICA=1|2
-// overrides (tests use it to check both paths agree bitwise).
-int ctas_per_replica(uint64_t rows, int sms, int entropy_kind) {
+// CTAs per replica: the CS in {1, 2, 4} (at most the replica's 64x64 tile count, but 2 is
+// always allowed) that leaves the fewest SMs idle, preferring fewer CTAs unless a larger CS
+// gains >= 2% of the machine: e.g. 512 replicas on 148 SMs -> 2 (86.5% -> 98.8%), 1..37
+// replicas -> 4. TG_HBM_CTAS_PER_REPLICA=1|2|4 overrides (tests check they agree bitwise).
+int ctas_per_replica(uint32_t spins, uint64_t rows, int sms, int entropy_kind) {
   if (entropy_kind == 0) return 1;  // von Neumann: the eigen-solver runs in one CTA
+  const int tiles = 1 << (2 * (static_cast<int>(spins) / 2 - 6));
   if (const char* env = std::getenv("TG_HBM_CTAS_PER_REPLICA")) {
     const int v = std::atoi(env);
-    if (v == 1 || v == 2) return v;
+    if (v == 1 || v == 2 || v == 4) return v;
   }
   if (rows == 0) return 1;
   auto eff = [&](uint64_t units) {
     const uint64_t waves = (units + sms - 1) / sms;
     return static_cast<double>(units) / static_cast<double>(waves * sms);
   };
-  return eff(2 * rows) > eff(rows) + 0.02 ? 2 : 1;
+  int best = 1;
+  for (int cs = 2; cs <= kMaxCS; cs *= 2)
+    if ((cs <= tiles || cs == 2) && eff(cs * rows) > eff(best * rows) + 0.02) best = cs;
+  return best;
 }
 
 }  // namespace hbm
@@ -409,7 +401,7 @@ int ctas_per_replica(uint64_t rows, int sms, int entropy_kind) {
 size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  const int cs = hbm::ctas_per_replica(rows, sms, entropy_kind);
+  const int cs = hbm::ctas_per_replica(spins, rows, sms, entropy_kind);
   const uint64_t clusters = std::min<uint64_t>(rows, static_cast<uint64_t>(sms / cs));
   const size_t da = size_t{1} << (spins / 2);
   // von Neumann with d_a > 64: rho (2 planes of d_a^2) after each slab (vn_packed.cuh)
@@ -424,7 +416,7 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int cs = hbm::ctas_per_replica(p.rows, sms, p.entropy_kind);
+  const int cs = hbm::ctas_per_replica(p.spins, p.rows, sms, p.entropy_kind);
   if (p.entropy_kind == 0 && p.spins > static_cast<uint32_t>(kVnMaxSpins)) return cudaErrorInvalidValue;
   const uint64_t clusters = std::min<uint64_t>(p.rows, static_cast<uint64_t>(sms / cs));
   const int grid = static_cast<int>(clusters) * cs;
@@ -433,7 +425,8 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   void (*kern)(AnnealParams);
   if (p.entropy_kind == 0) kern = trace ? hbm::anneal_hbm_kernel<true, 1, 1> : hbm::anneal_hbm_kernel<false, 1, 1>;
   else if (cs == 1) kern = trace ? hbm::anneal_hbm_kernel<true, 1, 0> : hbm::anneal_hbm_kernel<false, 1, 0>;
-  else kern = trace ? hbm::anneal_hbm_kernel<true, 2, 0> : hbm::anneal_hbm_kernel<false, 2, 0>;
+  else if (cs == 2) kern = trace ? hbm::anneal_hbm_kernel<true, 2, 0> : hbm::anneal_hbm_kernel<false, 2, 0>;
+  else kern = trace ? hbm::anneal_hbm_kernel<true, 4, 0> : hbm::anneal_hbm_kernel<false, 4, 0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};

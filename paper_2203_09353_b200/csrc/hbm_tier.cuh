@@ -8,9 +8,9 @@
 // 32-column chunks of the A (rows of tile i) and B (rows of tile j) panels, staged in
 // SMEM with pitch 68 doubles (conflict-free DMMA fragments). Each warp computes a 16x32
 // sub-tile (2x4 blocks of 8x8) with the real-split DMMA scheme; the epilogue folds
-// sum |rho_ij|^2 and trace(rho) into two running chains, even tiles and odd tiles, and rho
-// is never stored. Rank k of a 2-CTA cluster takes the tiles t = k (mod 2), i.e. exactly
-// one chain, so the result is bitwise the same whether 1 or 2 CTAs share a replica.
+// sum |rho_ij|^2 and trace(rho) into four canonical chains (tile t -> chain t mod 4), and
+// rho is never stored. Rank k of a CS-CTA cluster (CS = 1, 2, 4) takes the tiles
+// t = k (mod CS), i.e. whole chains, so the result is bitwise the same whatever CS is.
 #pragma once
 #include "smem_tier.cuh"
 
@@ -18,6 +18,7 @@ namespace tg {
 namespace hbm {
 
 constexpr int kWarps = 8;
+constexpr int kChains = 4;    // canonical reduction chains (tile t -> chain t % 4)
 constexpr int kThreads = kWarps * 32;
 constexpr int TB = 64;        // output tile (complex rows/cols)
 constexpr int KC = 32;        // K columns per pipeline stage
@@ -168,8 +169,8 @@ __device__ __forceinline__ void load_stage(const double* X, const double* Y, int
   }
 }
 
-// rho partials of the tiles t = first, first + stride, ... (rank's share), as two chains by
-// tile parity: out = {rho2_even, rho2_odd, tr_even, tr_odd}, warp-reduced (all lanes).
+// rho partials of the tiles t = first, first + stride, ... (rank's share), as kChains chains
+// by t mod 4: out = {rho2 chain 0..3, trace chain 0..3}, warp-reduced (all lanes).
 // inject_fault flips the sign of the first accumulation term of rho(0,0) (linalg.cpp:94)
 // after the trace is taken.
 // STORE (von Neumann, single tile d_a = TB only): after the pipeline drains, rho is also
@@ -177,15 +178,14 @@ __device__ __forceinline__ void load_stage(const double* X, const double* Y, int
 template <bool STORE = false>
 __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, const double* Y,
                                              double* stages, int tid, int warp, int lane,
-                                             int first, int stride, bool fault, double out[4],
+                                             int first, int stride, bool fault, double out[2 * kChains],
                                              double* Rr = nullptr, double* Ri = nullptr, int RP = 0,
                                              int64_t* prof = nullptr, double* Rg = nullptr) {
   // STORE with Rg (von Neumann, d_a > TB): every finished tile is written to the global
   // column-major planes Rg (Re) and Rg + d_a^2 (Im) instead of SMEM.
   // prof (profiling probe only, thread 0): [0] clk in the chunk waits + barriers,
-  // [1] clk in tile epilogues, [2] clk until the first chunk landed.
-  int64_t t_wait = 0, t_epi = 0, t_first = 0;
-  const int64_t t_start = prof ? clock64() : 0;
+  // [1] clk in tile epilogues, [2] the largest per-warp wait.
+  int64_t t_wait = 0, t_epi = 0;
   const int wr = warp / T8::WC, wc = warp % T8::WC;
   const int m = lane >> 2, kq = lane & 3;
   const int nk = G.kchunks(), nt = G.tiles();
@@ -197,7 +197,7 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-  double rho[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}}, tr[2] = {0.0, 0.0};
+  double rho[kChains] = {0.0, 0.0, 0.0, 0.0}, tr[kChains] = {0.0, 0.0, 0.0, 0.0};
   auto issue = [&](int it) {
     if (it < total) {
       const int t = first + (it / nk) * stride, kc = it % nk;
@@ -211,11 +211,7 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
     const int64_t tw0 = prof ? clock64() : 0;
     cp_async_wait<1>();       // this thread's copies of stage `it` landed
     consumer_sync(kThreads);  // everyone's did; stage (it-1) % 3 is free
-    if (prof) {
-      const int64_t tw1 = clock64();
-      t_wait += tw1 - tw0;
-      if (it == 0) t_first = tw1 - t_start;
-    }
+    if (prof) t_wait += clock64() - tw0;
     // stage it+2 is issued 2 copies per k-step, spread over the chunk's 8 k-steps (keeps
     // the LSU queue short). Its addresses are set up here, once per chunk, as 32-bit
     // offsets from X (Y = X + n): an address computation inside the k-steps sits on the
@@ -276,9 +272,11 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
     if (it % nk == nk - 1) {  // tile epilogue
       const int64_t te0 = prof ? clock64() : 0;
       const int t = first + (it / nk) * stride, ti = t / nt, tj = t % nt;
-      const bool odd = t & 1;  // chain by tile parity (selects, not a dynamic index: no local memory)
+      const int ch = t & (kChains - 1);  // chain (selects below, not a dynamic index: no local memory)
       if (ti == tj) {
-        double tsum = odd ? tr[1] : tr[0];
+        double tsum = 0.0;
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) tsum = c == ch ? tr[c] : tsum;
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -287,12 +285,11 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
               if (m == 2 * kq) tsum += cr[i][j][0];
               if (m == 2 * kq + 1) tsum += cr[i][j][1];
             }
-        if (odd) tr[1] = tsum; else tr[0] = tsum;
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) tr[c] = c == ch ? tsum : tr[c];
       }
       if (fault && t == 0 && wr == 0 && wc == 0 && lane == 0)
         cr[0][0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);
-      // four interleaved chains per parity: the fold is 8 DFMA deep instead of 32 (it runs
-      // next to other warps' DMMA streams, which starve FP64 latency chains)
       if (STORE && Rg) {
         const size_t pl = static_cast<size_t>(G.da) * G.da;
 #pragma unroll
@@ -307,9 +304,9 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
               __stcg(Rg + pl + o, ci[i][j][e]);
             }
       }
-      double acc[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[c] = odd ? rho[1][c] : rho[0][c];
+      // the tile's value in four interleaved sub-chains: the fold is 8 DFMA deep instead of
+      // 32 (it runs next to other warps' DMMA streams, which starve FP64 latency chains)
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -324,10 +321,9 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
               ci[i][j][e] = 0.0;
             }
           }
+      const double tv = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (odd) rho[1][c] = acc[c]; else rho[0][c] = acc[c];
-      }
+      for (int c = 0; c < kChains; ++c) rho[c] = c == ch ? rho[c] + tv : rho[c];
       if (prof) t_epi += clock64() - te0;
     }
   }
@@ -340,14 +336,15 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
       for (int w = 0; w < kWarps; ++w) mx = wwait[w] > mx ? wwait[w] : mx;
       prof[0] = t_wait;
       prof[1] = t_epi;
-      prof[2] = mx + 0 * t_first;
+      prof[2] = mx;
     }
   }
   cp_async_wait<0>();
-  out[0] = warp_sum((rho[0][0] + rho[0][1]) + (rho[0][2] + rho[0][3]));
-  out[1] = warp_sum((rho[1][0] + rho[1][1]) + (rho[1][2] + rho[1][3]));
-  out[2] = warp_sum(tr[0]);
-  out[3] = warp_sum(tr[1]);
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    out[c] = warp_sum(rho[c]);
+    out[kChains + c] = warp_sum(tr[c]);
+  }
   consumer_sync(kThreads);  // all warps done with the stages before they are reused
   if (STORE && !Rg) {
 #pragma unroll

@@ -320,17 +320,18 @@ def test_zero_steps_and_single_replica(device):
 
 @pytest.mark.parametrize("spins,procs,steps", [(14, 5, 20), (16, 3, 6), (13, 4, 12)])
 def test_hbm_cluster_split_bitwise(device, oracle, spins, procs, steps, monkeypatch):
-    """HBM tier: one replica per CTA and one replica per 2-CTA cluster (rank k takes the
-    tiles of parity k, partial sums exchanged through DSMEM) produce bitwise-identical traces
-    (canonical even/odd chain order), and both match the oracle."""
+    """HBM tier: one replica per CTA, per 2-CTA and per 4-CTA cluster (rank k takes the
+    tiles t = k mod CS, chain sums exchanged through DSMEM) produce bitwise-identical traces
+    (four canonical chains, canonical renormalisation quarters), and match the oracle."""
     cfg = tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=8, initial_state="random")
     monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", "1")
     a = device.run(cfg)
-    monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", "2")
-    b = device.run(cfg)
-    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
-    assert np.array_equal(a.accepted, b.accepted)
-    assert np.array_equal(a.initial_entropy.view(np.uint64), b.initial_entropy.view(np.uint64))
+    for cs in ("2", "4"):
+        monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", cs)
+        b = device.run(cfg)
+        assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64)), cs
+        assert np.array_equal(a.accepted, b.accepted), cs
+        assert np.array_equal(a.initial_entropy.view(np.uint64), b.initial_entropy.view(np.uint64)), cs
     want = oracle.run(McCfg(spins=spins, steps=steps, seed=8, initial_state=1), 0, procs)
     assert np.array_equal(b.accepted, want.accepted)
     assert close(b.entropies, want.entropies).all()

@@ -34,5 +34,7 @@ if spins >= 13:  # HBM tier: GEMM-internal clocks (thread 0)
         "  GEMM: max per-warp chunk waits": s[:, 6],
     })
 print(f"S={spins} replicas={replicas} steps={steps}")
+import signal
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 for k, v in rows.items():
     print(f"  {k:32s} median {np.median(v):8.0f} clk   mean {np.mean(v):8.0f}")
