@@ -171,7 +171,7 @@ tg_status tg_probe_apply_gate(uint32_t spins, const double* psi, int site, const
 tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* entropy,
                            double* norms);
 /* same with the entropy kind (tg_entropy_kind): TG_VON_NEUMANN = eigenvalues of rho on the
- * device (spins <= 12), spinmc.cpp:165-169 / linalg.cpp:161-232 */
+ * device (spins <= 15), spinmc.cpp:165-169 / linalg.cpp:161-232 */
 tg_status tg_probe_entropy_kind(uint32_t spins, uint64_t count, const double* psi, int32_t kind,
                                 double* entropy, double* norms);
 
@@ -179,6 +179,15 @@ tg_status tg_probe_entropy_kind(uint32_t spins, uint64_t count, const double* ps
  * first replica, trace[steps][8]: 0 step start, 1 gate pass done, 2 GEMM done,
  * 3 decision done. */
 tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* trace);
+
+/* Test probe: the proposal pre-pass's chunked jump-ahead RNG (per replica, chunks of 256
+ * steps start from xoshiro256++ states advanced by GF(2) matrix powers; rng.cpp:35-59)
+ * against one sequential stream per replica, seeds derive_stream({0, p}), p < rows.
+ * reject_below: the uniform_index rejection threshold (0 = the reference's
+ * (2^64 - n) mod n; larger values force rejections and exercise the fixup pass).
+ * *mismatches = number of differing draw words + sites (0 = identical). */
+tg_status tg_probe_rng_chunking(uint32_t spins, uint64_t rows, uint64_t steps, int32_t random_init,
+                                uint64_t reject_below, uint64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -100,7 +100,8 @@ EXPORTS = [
     "tg_anneal_rows", "tg_step_flops", "tg_anneal_run", "tg_anneal_launch",
     "tg_anneal_workspace_bytes", "tg_zgemm_batched", "tg_zgemm_strided_launch",
     "tg_fp64_dmma_peak", "tg_probe_rng", "tg_probe_gates", "tg_probe_apply_gate",
-    "tg_probe_entropy", "tg_probe_entropy_kind", "tg_probe_phase_trace", "tg_set_perturb_gemm",
+    "tg_probe_entropy", "tg_probe_entropy_kind", "tg_probe_phase_trace", "tg_probe_rng_chunking",
+    "tg_set_perturb_gemm",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -146,6 +147,8 @@ def lib() -> C.CDLL:
     L.tg_probe_entropy_kind.argtypes = [C.c_uint32, C.c_uint64, _dp, C.c_int32, _dp, _dp]
     L.tg_set_perturb_gemm.argtypes = [C.c_int]
     L.tg_probe_phase_trace.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64)]
+    L.tg_probe_rng_chunking.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int32, C.c_uint64,
+                                        C.POINTER(C.c_uint64)]
     for name in EXPORTS:
         if name not in ("tg_last_error", "tg_version", "tg_kernel_launches", "tg_anneal_rows", "tg_step_flops",
                         "tg_anneal_workspace_bytes"):
@@ -425,6 +428,15 @@ def probe_phase_trace(spins: int, replicas: int, steps: int) -> np.ndarray:
     out = np.zeros((steps, 8), np.int64)
     _check(lib().tg_probe_phase_trace(spins, replicas, steps, out.ctypes.data_as(C.POINTER(C.c_int64))))
     return out
+
+
+def probe_rng_chunking(spins: int, rows: int, steps: int, random_init: bool = False,
+                       reject_below: int = 0) -> int:
+    """Differing draw words + sites between the chunked jump-ahead pre-pass and one
+    sequential stream per replica (0 = identical); reject_below > 0 forces rejections."""
+    mm = C.c_uint64()
+    _check(lib().tg_probe_rng_chunking(spins, rows, steps, int(random_init), reject_below, C.byref(mm)))
+    return int(mm.value)
 
 
 def kernel_launches() -> int:

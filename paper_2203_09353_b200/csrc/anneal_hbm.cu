@@ -12,6 +12,7 @@
 // Every FP64 op outside the GEMM runs while no DMMA is in flight on the SM (the FP64 pipe
 // is shared, profiles/r01_fp64_contention.txt). The proposal stream comes from the
 // pre-pass (gate_stream.cu).
+#include <cstdio>
 #include <cstdlib>
 
 #include "hbm_tier.cuh"
@@ -374,10 +375,13 @@ cudaError_t probe_entropy(uint32_t spins, uint64_t count, const double* psi, dou
   return e;
 }
 
-// CTAs per replica: the CS in {1, 2, 4} (at most the replica's 64x64 tile count, but 2 is
-// always allowed) that leaves the fewest SMs idle, preferring fewer CTAs unless a larger CS
-// gains >= 2% of the machine: e.g. 512 replicas on 148 SMs -> 2 (86.5% -> 98.8%), 1..37
-// replicas -> 4. TG_HBM_CTAS_PER_REPLICA=1|2|4 overrides (tests check they agree bitwise).
+// CTAs per replica. Small batches (cs * rows <= SMs for some cs > 1): the largest cs in
+// {2, 4} (at most the replica's 64x64 tile count, 2 always allowed) that still fits one
+// wave, since otherwise SMs idle. Larger batches: 1, or 2 when that removes a partial last
+// wave worth >= 2% of the machine (e.g. 512 replicas on 148 SMs: 86.5% -> 98.8%). A
+// 4-CTA replica is far less efficient per SM than a 1-CTA one (one 64x64 tile per CTA at
+// S = 14: fixed per-step costs dominate), so it is only worth it while SMs would idle.
+// TG_HBM_CTAS_PER_REPLICA=1|2|4 overrides (tests check they agree bitwise).
 int ctas_per_replica(uint32_t spins, uint64_t rows, int sms, int entropy_kind) {
   if (entropy_kind == 0) return 1;  // von Neumann: the eigen-solver runs in one CTA
   const int tiles = 1 << (2 * (static_cast<int>(spins) / 2 - 6));
@@ -386,23 +390,90 @@ int ctas_per_replica(uint32_t spins, uint64_t rows, int sms, int entropy_kind) {
     if (v == 1 || v == 2 || v == 4) return v;
   }
   if (rows == 0) return 1;
+  for (int cs = kMaxCS; cs >= 2; cs /= 2)
+    if ((cs <= tiles || cs == 2) && static_cast<uint64_t>(cs) * rows <= static_cast<uint64_t>(sms)) return cs;
   auto eff = [&](uint64_t units) {
     const uint64_t waves = (units + sms - 1) / sms;
     return static_cast<double>(units) / static_cast<double>(waves * sms);
   };
-  int best = 1;
-  for (int cs = 2; cs <= kMaxCS; cs *= 2)
-    if ((cs <= tiles || cs == 2) && eff(cs * rows) > eff(best * rows) + 0.02) best = cs;
-  return best;
+  return eff(2 * rows) > eff(rows) + 0.02 ? 2 : 1;
 }
 
 }  // namespace hbm
 
-size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind) {
+namespace {
+
+using HbmKernel = void (*)(AnnealParams);
+HbmKernel hbm_kernel(int kind, int cs, bool trace) {
+  if (kind == 0) return trace ? hbm::anneal_hbm_kernel<true, 1, 1> : hbm::anneal_hbm_kernel<false, 1, 1>;
+  if (cs == 1) return trace ? hbm::anneal_hbm_kernel<true, 1, 0> : hbm::anneal_hbm_kernel<false, 1, 0>;
+  if (cs == 2) return trace ? hbm::anneal_hbm_kernel<true, 2, 0> : hbm::anneal_hbm_kernel<false, 2, 0>;
+  return trace ? hbm::anneal_hbm_kernel<true, 4, 0> : hbm::anneal_hbm_kernel<false, 4, 0>;
+}
+
+cudaLaunchConfig_t hbm_config(int grid, int cs, cudaStream_t stream, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(hbm::kThreads);
+  cfg.dynamicSmemBytes = hbm::kSmemBytes;
+  cfg.stream = stream;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+// CTAs per replica and the number of persistent clusters: at most the clusters that can
+// be co-resident (a GPC whose SM count is not a multiple of cs leaves SMs over, so 4-CTA
+// clusters do not reach sms / 4: a non-resident cluster would run as a second wave).
+cudaError_t hbm_geometry(uint32_t spins, uint64_t rows, int kind, int device, int& cs, uint64_t& clusters) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  const int cs = hbm::ctas_per_replica(spins, rows, sms, entropy_kind);
-  const uint64_t clusters = std::min<uint64_t>(rows, static_cast<uint64_t>(sms / cs));
+  auto resident_for = [&](int c, int& resident) -> cudaError_t {
+    resident = sms / c;
+    if (c == 1) return cudaSuccess;
+    HbmKernel kern = hbm_kernel(kind, c, false);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = hbm_config(resident * c, c, nullptr, attr);
+    int n = 0;
+    e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+    if (e != cudaSuccess) return e;
+    if (n > 0 && n < resident) resident = n;
+    return cudaSuccess;
+  };
+  cs = hbm::ctas_per_replica(spins, rows, sms, kind);
+  int resident = 0;
+  cudaError_t e = resident_for(cs, resident);
+  if (e != cudaSuccess) return e;
+  // a small batch that does not fit the co-resident 4-CTA clusters drops to 2 CTAs (unless
+  // forced by TG_HBM_CTAS_PER_REPLICA)
+  if (cs == 4 && rows > static_cast<uint64_t>(resident) && !std::getenv("TG_HBM_CTAS_PER_REPLICA")) {
+    cs = 2;
+    e = resident_for(cs, resident);
+    if (e != cudaSuccess) return e;
+  }
+  clusters = std::min<uint64_t>(rows, static_cast<uint64_t>(resident));
+  if (std::getenv("TG_VERBOSE"))
+    std::fprintf(stderr, "[tg] hbm geometry: spins %u rows %llu -> %d CTAs/replica, %llu clusters (resident %d)\n",
+                 spins, static_cast<unsigned long long>(rows), cs, static_cast<unsigned long long>(clusters), resident);
+  return cudaSuccess;
+}
+
+}  // namespace
+
+size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind) {
+  int cs = 1;
+  uint64_t clusters = 0;
+  if (hbm_geometry(spins, rows, entropy_kind, device, cs, clusters) != cudaSuccess) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    clusters = std::min<uint64_t>(rows, static_cast<uint64_t>(sms));  // upper bound
+  }
   const size_t da = size_t{1} << (spins / 2);
   // von Neumann with d_a > 64: rho (2 planes of d_a^2) after each slab (vn_packed.cuh)
   const size_t rho = entropy_kind == 0 && da > static_cast<size_t>(hbm::TB) ? 2 * da * da : 0;
@@ -413,34 +484,20 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
                               bool trace) {
   if (p.spins < 13 || p.spins > 24) return cudaErrorInvalidValue;
   if (!p.workspace) return cudaErrorInvalidValue;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int cs = hbm::ctas_per_replica(p.spins, p.rows, sms, p.entropy_kind);
   if (p.entropy_kind == 0 && p.spins > static_cast<uint32_t>(kVnMaxSpins)) return cudaErrorInvalidValue;
-  const uint64_t clusters = std::min<uint64_t>(p.rows, static_cast<uint64_t>(sms / cs));
+  int dev = 0, cs = 1;
+  uint64_t clusters = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = hbm_geometry(p.spins, p.rows, p.entropy_kind, dev, cs, clusters);
+  if (e != cudaSuccess) return e;
   const int grid = static_cast<int>(clusters) * cs;
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
-  void (*kern)(AnnealParams);
-  if (p.entropy_kind == 0) kern = trace ? hbm::anneal_hbm_kernel<true, 1, 1> : hbm::anneal_hbm_kernel<false, 1, 1>;
-  else if (cs == 1) kern = trace ? hbm::anneal_hbm_kernel<true, 1, 0> : hbm::anneal_hbm_kernel<false, 1, 0>;
-  else if (cs == 2) kern = trace ? hbm::anneal_hbm_kernel<true, 2, 0> : hbm::anneal_hbm_kernel<false, 2, 0>;
-  else kern = trace ? hbm::anneal_hbm_kernel<true, 4, 0> : hbm::anneal_hbm_kernel<false, 4, 0>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
+  HbmKernel kern = hbm_kernel(p.entropy_kind, cs, trace);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
   if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(hbm::kThreads);
-  cfg.dynamicSmemBytes = hbm::kSmemBytes;
-  cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cudaLaunchConfig_t cfg = hbm_config(grid, cs, stream, attr);
   e = cudaLaunchKernelEx(&cfg, kern, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -164,7 +164,7 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
     tg::GateStream gs{};
     cudaError_t e = tg::launch_gate_stream(q, base, stream_bytes, &gs, s);
     if (e != cudaSuccess) return e;
-    g_launches += p.initial_state == 1 ? 3 : 2;  // rng_draws, gate_convert (, init_convert)
+    g_launches += p.initial_state == 1 ? 4 : 3;  // rng_chunk, rng_fixup, gate_convert (, init_convert)
     q.gates = gs.recs;
     q.init_states = gs.init_states;
     q.workspace = reinterpret_cast<double*>(slabs);
@@ -585,6 +585,14 @@ tg_status tg_probe_entropy_kind(uint32_t spins, uint64_t count, const double* ps
 tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, double* entropy,
                            double* norms) {
   return tg_probe_entropy_kind(spins, count, psi, TG_RENYI2, entropy, norms);
+}
+
+tg_status tg_probe_rng_chunking(uint32_t spins, uint64_t rows, uint64_t steps, int32_t random_init,
+                                uint64_t reject_below, uint64_t* mismatches) {
+  if (!mismatches) return fail(TG_EINVAL, "mismatches must not be NULL");
+  if (spins < 3 || spins > 24 || rows == 0) return fail(TG_EINVAL, "probe_rng_chunking: spins in [3,24], rows > 0");
+  TG_CUDA(tg::probe_rng_chunking(spins, rows, steps, random_init, reject_below, mismatches));
+  return TG_OK;
 }
 
 tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* trace) {

@@ -40,6 +40,8 @@ struct GateStream {
   double* init_states;
 };
 size_t gate_stream_bytes_per_row(uint32_t spins, uint64_t steps, int random_init);
+cudaError_t probe_rng_chunking(uint32_t spins, uint64_t rows, uint64_t steps, int random_init,
+                               uint64_t reject_below, uint64_t* mismatches);
 cudaError_t launch_gate_stream(const AnnealParams& p, void* ws, size_t ws_bytes, GateStream* gs,
                                cudaStream_t stream);
 

@@ -49,6 +49,18 @@ def test_t2_t3_gate_stream(oracle, spins, initial):
     assert np.median(ulp) <= 4
 
 
+@pytest.mark.parametrize("spins,rows,steps,random_init,reject_below", [
+    (12, 37, 1000, False, 0),          # 4 chunks, the reference threshold (no rejection)
+    (8, 5, 700, True, 0),              # random-start draws before the steps (T^(2^(S+1)) jump)
+    (12, 9, 900, False, 1 << 62),      # forced rejections: every replica takes the fixup path
+    (5, 3, 300, True, (1 << 63) + 5),  # forced rejections after random-start draws
+])
+def test_t2_rng_chunked_jump_ahead(spins, rows, steps, random_init, reject_below):
+    """The pre-pass's chunked xoshiro256++ (chunks of 256 steps started by GF(2) jump
+    matrices, rejection fixup) reproduces one sequential stream per replica word for word."""
+    assert tg.probe_rng_chunking(spins, rows, steps, random_init, reject_below) == 0
+
+
 # ------------------------------------------------------------------- T4 gate application
 # S <= 12 applies the gate in fused (DFMA) form — DMMA and DFMA share the FP64 pipe on
 # sm_100a, so halving the gate's op count is worth ~6% of the step (DESIGN.md §3): within
