@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   const bool writer = rank == 0;
 
   for (uint64_t r = cid; r < P.rows; r += ncl) {
-    const GateRec* recs = P.gates + r * P.steps;
+    const GateRec* recs = P.gates + r;  // record s at recs[s * rows] (gate_stream.cu layout)
     {  // initial state, split by halves of the amplitude index
       const int i0 = static_cast<int>(rank) * (G.n / CS), i1 = i0 + G.n / CS;
       if (P.initial_state == 0) {
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     int64_t t_prev = (tid == 0 && P.wall_ns) ? globaltimer() : 0;
     uint64_t renorm_left = P.renorm;  // countdown: no 64-bit modulo per step
     for (uint64_t s = 0; s < P.steps && !err; ++s) {
-      const GateRec& g = recs[s];
+      const GateRec& g = recs[s * P.rows];
       mark(r, s, 0);
       gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, kThreads);
       __threadfence();
