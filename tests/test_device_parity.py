@@ -248,6 +248,24 @@ def test_t7_von_neumann_packed_vs_oracle(device, oracle, spins, objective):
     assert close(rep.initial_entropy, want.initial).all()
 
 
+@pytest.mark.slow
+def test_t7_config4_shape_vs_oracle(device, oracle, monkeypatch):
+    """BASELINE config 4's chain (L=20, 1024x1024x1024 complex GEMMs): a replica's initial
+    entropy and first steps against the oracle (the reference's O(d^3) GEMM, ~7 s per step
+    on one core), on one CTA and on a 4-CTA cluster (bitwise equal)."""
+    cfg = tg.ExperimentConfig(spins=20, steps=2, procedures=1, seed=4)
+    want = oracle.run(McCfg(spins=20, steps=2, seed=4), 0, 1)
+    monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", "1")
+    a = device.run(cfg)
+    monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", "4")
+    b = device.run(cfg)
+    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
+    assert np.array_equal(a.sites, want.sites)
+    assert np.array_equal(a.accepted, want.accepted)
+    assert close(a.entropies, want.entropies).all(), np.max(np.abs(a.entropies - want.entropies))
+    assert close(a.initial_entropy, want.initial).all()
+
+
 def test_t7_von_neumann_appendix_a(device):
     rep = device.run(cfg_from(load_traj("vn_cfg1")))
     assert int(rep.accepted.sum()) == 59795
