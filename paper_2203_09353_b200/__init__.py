@@ -101,6 +101,7 @@ EXPORTS = [
     "tg_anneal_workspace_bytes", "tg_zgemm_batched", "tg_zgemm_strided_launch",
     "tg_fp64_dmma_peak", "tg_probe_rng", "tg_probe_gates", "tg_probe_apply_gate",
     "tg_probe_entropy", "tg_probe_entropy_kind", "tg_probe_phase_trace", "tg_probe_rng_chunking",
+    "tg_rng_jump_words",
     "tg_set_perturb_gemm",
 ]
 
@@ -149,6 +150,8 @@ def lib() -> C.CDLL:
     L.tg_probe_phase_trace.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64)]
     L.tg_probe_rng_chunking.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int32, C.c_uint64,
                                         C.POINTER(C.c_uint64)]
+    L.tg_rng_jump_words.argtypes = [C.c_uint64, C.c_uint64, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64,
+                                    C.POINTER(C.c_uint64)]
     for name in EXPORTS:
         if name not in ("tg_last_error", "tg_version", "tg_kernel_launches", "tg_anneal_rows", "tg_step_flops",
                         "tg_anneal_workspace_bytes"):
@@ -437,6 +440,13 @@ def probe_rng_chunking(spins: int, rows: int, steps: int, random_init: bool = Fa
     mm = C.c_uint64()
     _check(lib().tg_probe_rng_chunking(spins, rows, steps, int(random_init), reject_below, C.byref(mm)))
     return int(mm.value)
+
+
+def rng_jump_words(seed: int, p: int, chunks: int, extra: int = 0, n: int = 4, init_spins: int = -1) -> np.ndarray:
+    """Host (no GPU): stream words after the pre-pass's GF(2) jumps (tg_rng_jump_words)."""
+    out = np.zeros(n, np.uint64)
+    _check(lib().tg_rng_jump_words(seed, p, init_spins, chunks, extra, n, out.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return out
 
 
 def kernel_launches() -> int:

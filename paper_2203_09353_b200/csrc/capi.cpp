@@ -587,6 +587,14 @@ tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, do
   return tg_probe_entropy_kind(spins, count, psi, TG_RENYI2, entropy, norms);
 }
 
+tg_status tg_rng_jump_words(uint64_t seed, uint64_t p, int32_t init_spins, uint64_t chunks, uint64_t extra,
+                            uint64_t n, uint64_t* out) {
+  if (!out && n) return fail(TG_EINVAL, "out must not be NULL");
+  if (init_spins > 24 || chunks >= (uint64_t{1} << 16)) return fail(TG_EINVAL, "rng_jump_words: init_spins <= 24, chunks < 2^16");
+  tg::rng_jump_words(seed, p, init_spins, chunks, extra, n, out);
+  return TG_OK;
+}
+
 tg_status tg_probe_rng_chunking(uint32_t spins, uint64_t rows, uint64_t steps, int32_t random_init,
                                 uint64_t reject_below, uint64_t* mismatches) {
   if (!mismatches) return fail(TG_EINVAL, "mismatches must not be NULL");

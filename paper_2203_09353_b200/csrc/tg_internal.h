@@ -40,6 +40,8 @@ struct GateStream {
   double* init_states;
 };
 size_t gate_stream_bytes_per_row(uint32_t spins, uint64_t steps, int random_init);
+void rng_jump_words(uint64_t seed, uint64_t p, int init_spins, uint64_t chunks, uint64_t extra, uint64_t n,
+                    uint64_t* out);
 cudaError_t probe_rng_chunking(uint32_t spins, uint64_t rows, uint64_t steps, int random_init,
                                uint64_t reject_below, uint64_t* mismatches);
 cudaError_t launch_gate_stream(const AnnealParams& p, void* ws, size_t ws_bytes, GateStream* gs,

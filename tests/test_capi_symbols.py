@@ -5,6 +5,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 import paper_2203_09353_b200 as tg
@@ -98,3 +99,15 @@ def test_batched_gemm_contract_errors_host_side():
         d.batched_gemm([np.zeros((2, 3)), np.zeros((3, 3))], [np.zeros((3, 2)), np.zeros((3, 2))])
     with pytest.raises(ValueError, match=re.escape("A.cols (3) != B.rows (4)")):
         d.batched_gemm([np.zeros((2, 3))], [np.zeros((4, 2))])
+
+
+@pytest.mark.parametrize("seed,p,init_spins,chunks,extra", [
+    (0, 0, -1, 1, 0), (0, 3, -1, 5, 7), (11, 1, -1, 37, 100), (5, 2, 4, 0, 0), (5, 2, 6, 3, 2), (9, 0, 8, 2, 33)])
+def test_rng_jump_tables_vs_sequential_stream(oracle, seed, p, init_spins, chunks, extra):
+    """The pre-pass's GF(2) jump tables (host copy of what rng_chunk_kernel uploads) land on
+    the same xoshiro256++ words as stepping the reference's stream (rng.cpp:23-45) one draw
+    at a time: chunk jumps of 34 * 256 draws and the random-start jump of 2^(S+1) draws."""
+    skip = (2 << init_spins if init_spins >= 0 else 0) + chunks * 34 * 256 + extra
+    want = oracle.first_u64(seed, p, skip + 8)[skip:]
+    got = tg.rng_jump_words(seed, p, chunks, extra, 8, init_spins)
+    assert np.array_equal(got, want)
