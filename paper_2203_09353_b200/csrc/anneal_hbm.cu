@@ -130,10 +130,13 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   if (packed) Rg = P.workspace + static_cast<size_t>(blockIdx.x) * (4 * static_cast<size_t>(G0.n) +
                                                                     2 * static_cast<size_t>(G0.da) * G0.da) +
                    4 * static_cast<size_t>(G0.n);
-  // entropy of the proposal whose rho the last GEMM produced (valid in thread 0)
+  // KIND 0: the trace value of a proposal is its raw ||rho||_F^2 (finish_renyi_kernel turns
+  // it into -log(f*f) after the kernel, as in the SMEM tier) and the decision is the lean
+  // smem::decide on rho2 (one multiply, reference formula near ties). KIND 1: the entropy
+  // of the proposal whose rho the last GEMM produced (valid in thread 0).
   auto entropy_of = [&](double rho2) -> double {
     if constexpr (KIND == 0) {
-      return smem::renyi2(rho2);
+      return rho2;
     } else {
       if (packed) {
         double* Ar = stages;
@@ -235,8 +238,12 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
         } else {
           H.error = 0;
           const double proposed = e_new;
-          const double delta = P.objective == 0 ? proposed - cur_e : cur_e - proposed;
-          acc = g.u < acceptance(delta, g.temp);
+          if constexpr (KIND == 0) {
+            acc = smem::decide(proposed, cur_e, g, P.objective);
+          } else {  // spinmc.cpp:203-207 verbatim
+            const double delta = P.objective == 0 ? proposed - cur_e : cur_e - proposed;
+            acc = g.u < acceptance(delta, g.temp);
+          }
           if (acc) cur_e = proposed;
         }
         H.decision = acc;
@@ -500,7 +507,9 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   cudaLaunchConfig_t cfg = hbm_config(grid, cs, stream, attr);
   e = cudaLaunchKernelEx(&cfg, kern, p);
   if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess || p.entropy_kind == 0) return e;
+  return launch_finish_renyi(p, stream);  // Renyi-2 traces were stored as raw ||rho||_F^2
 }
 
 }  // namespace tg

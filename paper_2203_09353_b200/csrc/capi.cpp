@@ -171,8 +171,8 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
     e = p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::launch_anneal_smem(q, s, nullptr, trace)
                                                            : tg::launch_anneal_hbm(q, s, nullptr, trace);
     if (e != cudaSuccess) return e;
-    // anneal kernel (+ finish_renyi_kernel in the SMEM tier's Renyi-2 path)
-    g_launches += (p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) && p.entropy_kind == TG_RENYI2) ? 2 : 1;
+    // anneal kernel (+ finish_renyi_kernel for Renyi-2: traces are stored as raw ||rho||_F^2)
+    g_launches += p.entropy_kind == TG_RENYI2 ? 2 : 1;
   }
   return cudaSuccess;
 }

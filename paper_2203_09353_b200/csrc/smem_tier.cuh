@@ -376,6 +376,22 @@ __device__ __forceinline__ double renyi2(double rho2) {
   return (e < 0.0) ? 0.0 : e;
 }
 
+// Metropolis decision of spinmc.cpp:201-207 on rho2 = ||rho||_F^2 (entropy = -log rho2,
+// clamped at 0 <=> rho2 clamped at 1): accept <=> u < exp(clamp(delta/T))
+// <=> delta > T log u <=> rho2' < rho2_cur * exp(-T log u) (maximize) or
+// rho2' > rho2_cur * exp(T log u) (minimize); emul is that factor. Relative margins below
+// 1e-12 are re-decided with the reference formula (entropies and exp), so the outcome is
+// the reference's wherever FP64 rounding cannot tie.
+template <class R>
+__device__ __forceinline__ int decide(double rho2_new, double rho2_cur, const R& g, int objective) {
+  const double r_new = fmin(rho2_new, 1.0), r_cur = fmin(rho2_cur, 1.0);
+  const double bound = r_cur * g.emul;
+  if (fabs(r_new - bound) > 1e-12 * r_new) return objective == 0 ? (r_new < bound) : (r_new > bound);
+  const double proposed = renyi2(rho2_new), current = renyi2(rho2_cur);
+  const double delta = objective == 0 ? proposed - current : current - proposed;
+  return g.u < acceptance(delta, g.temp);
+}
+
 // Norm check of spinmc.cpp:152-156 on trace(rho) = ||psi'||^2.
 __device__ __forceinline__ bool not_normalized(double trace) {
   return fabs(__dsqrt_rn(trace) - 1.0) > 1e-9;

@@ -59,6 +59,7 @@ cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* 
 // anneal_hbm.cu (S >= 13)
 cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out,
                               bool trace = false);
+cudaError_t launch_finish_renyi(const AnnealParams& p, cudaStream_t stream);
 size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind);
 
 // probes.cu
