@@ -249,6 +249,23 @@ def test_t7_von_neumann_packed_vs_oracle(device, oracle, spins, objective):
 
 
 @pytest.mark.slow
+def test_hbm_renormalisation_vs_oracle(device, oracle, monkeypatch):
+    """HBM tier across the every-1000-steps renormalisation (spinmc.cpp:246-248; canonical
+    quarter sums) on one CTA and on a 4-CTA cluster: bitwise equal, and equal to the oracle
+    (sites, accept flags bit-exact; entropies within 1e-10)."""
+    cfg = tg.ExperimentConfig(spins=14, steps=1010, procedures=1, seed=6)
+    want = oracle.run(McCfg(spins=14, steps=1010, seed=6), 0, 1)
+    monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", "1")
+    a = device.run(cfg)
+    monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", "4")
+    b = device.run(cfg)
+    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
+    assert np.array_equal(a.sites, want.sites)
+    assert np.array_equal(a.accepted, want.accepted)
+    assert close(a.entropies, want.entropies).all(), np.max(np.abs(a.entropies - want.entropies))
+
+
+@pytest.mark.slow
 def test_t7_config4_shape_vs_oracle(device, oracle, monkeypatch):
     """BASELINE config 4's chain (L=20, 1024x1024x1024 complex GEMMs): a replica's initial
     entropy and first steps against the oracle (the reference's O(d^3) GEMM, ~7 s per step
