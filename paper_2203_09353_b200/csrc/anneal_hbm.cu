@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     }
   };
   int64_t* gprof = nullptr;  // TRACE: GEMM-internal clocks of the current step (slots 4..6)
-  auto gemm = [&](const double* X, const double* Y, int first, int stride, double out[4]) {
+  auto gemm = [&](const double* X, const double* Y, int first, int stride, double out[2 * kChains]) {
     const int tid = threadIdx.x;
     rho_partials<KIND == 1>(Geo(static_cast<int>(P.spins)), X, Y, stages, tid, tid >> 5, tid & 31, first,
                             stride, P.inject_fault != 0, out, Rr, Ri, kRP, gprof, Rg);

@@ -57,14 +57,6 @@ struct Tile {
   static_assert(WR * WC <= kConsumerWarps, "tiling");
 };
 
-struct Header {  // HBM tier CTA scratch
-  double part_rho[kConsumerWarps];
-  double part_tr[kConsumerWarps];
-  int32_t decision;
-  int32_t error;
-};
-constexpr int kHeaderBytes = (static_cast<int>(sizeof(Header)) + 127) / 128 * 128;
-
 // Gate application (spinmc.cpp:91-136) planar SMEM -> planar SMEM, fused form:
 // re = fma(-ui, vi, fma(ur, vr, re)); im = fma(ui, vr, fma(ur, vi, im)) over the four inputs
 // (in a lane-rotated order, below).
