@@ -189,10 +189,12 @@ tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps
 tg_status tg_probe_rng_chunking(uint32_t spins, uint64_t rows, uint64_t steps, int32_t random_init,
                                 uint64_t reject_below, uint64_t* mismatches);
 
+/* Steps per chunk of the pre-pass's jump-ahead RNG (each chunk is 34 * that many draws). */
+uint64_t tg_rng_chunk_steps(void);
 /* Host only (no GPU): the n words of derive_stream({seed, p}) (rng.cpp:23-45) after the
  * pre-pass's jumps: 2^(init_spins+1) draws when init_spins >= 0 (random start), then
- * chunks * 34 * 256 draws, then `extra` single draws — the jump tables rng_chunk_kernel
- * uses, so tests can check them against a sequential stream on the CPU. */
+ * chunks * 34 * tg_rng_chunk_steps() draws, then `extra` single draws — the jump tables
+ * rng_chunk_kernel uses, so tests can check them against a sequential stream on the CPU. */
 tg_status tg_rng_jump_words(uint64_t seed, uint64_t p, int32_t init_spins, uint64_t chunks, uint64_t extra,
                             uint64_t n, uint64_t* out);
 

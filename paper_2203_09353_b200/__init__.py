@@ -101,7 +101,7 @@ EXPORTS = [
     "tg_anneal_workspace_bytes", "tg_zgemm_batched", "tg_zgemm_strided_launch",
     "tg_fp64_dmma_peak", "tg_probe_rng", "tg_probe_gates", "tg_probe_apply_gate",
     "tg_probe_entropy", "tg_probe_entropy_kind", "tg_probe_phase_trace", "tg_probe_rng_chunking",
-    "tg_rng_jump_words",
+    "tg_rng_jump_words", "tg_rng_chunk_steps",
     "tg_set_perturb_gemm",
 ]
 
@@ -150,6 +150,7 @@ def lib() -> C.CDLL:
     L.tg_probe_phase_trace.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64)]
     L.tg_probe_rng_chunking.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int32, C.c_uint64,
                                         C.POINTER(C.c_uint64)]
+    L.tg_rng_chunk_steps.restype = C.c_uint64
     L.tg_rng_jump_words.argtypes = [C.c_uint64, C.c_uint64, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64,
                                     C.POINTER(C.c_uint64)]
     for name in EXPORTS:

@@ -164,7 +164,7 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
     tg::GateStream gs{};
     cudaError_t e = tg::launch_gate_stream(q, base, stream_bytes, &gs, s);
     if (e != cudaSuccess) return e;
-    g_launches += p.initial_state == 1 ? 4 : 3;  // rng_chunk, rng_fixup, gate_convert (, init_convert)
+    g_launches += p.initial_state == 1 ? 3 : 2;  // rng_chunk (fused records), rng_fixup (, init_convert)
     q.gates = gs.recs;
     q.init_states = gs.init_states;
     q.workspace = reinterpret_cast<double*>(slabs);
@@ -586,6 +586,8 @@ tg_status tg_probe_entropy(uint32_t spins, uint64_t count, const double* psi, do
                            double* norms) {
   return tg_probe_entropy_kind(spins, count, psi, TG_RENYI2, entropy, norms);
 }
+
+uint64_t tg_rng_chunk_steps(void) { return tg::rng_chunk_steps(); }
 
 tg_status tg_rng_jump_words(uint64_t seed, uint64_t p, int32_t init_spins, uint64_t chunks, uint64_t extra,
                             uint64_t n, uint64_t* out) {

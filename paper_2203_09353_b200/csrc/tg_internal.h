@@ -40,6 +40,7 @@ struct GateStream {
   double* init_states;
 };
 size_t gate_stream_bytes_per_row(uint32_t spins, uint64_t steps, int random_init);
+uint64_t rng_chunk_steps();
 void rng_jump_words(uint64_t seed, uint64_t p, int init_spins, uint64_t chunks, uint64_t extra, uint64_t n,
                     uint64_t* out);
 cudaError_t probe_rng_chunking(uint32_t spins, uint64_t rows, uint64_t steps, int random_init,

@@ -106,8 +106,9 @@ def test_batched_gemm_contract_errors_host_side():
 def test_rng_jump_tables_vs_sequential_stream(oracle, seed, p, init_spins, chunks, extra):
     """The pre-pass's GF(2) jump tables (host copy of what rng_chunk_kernel uploads) land on
     the same xoshiro256++ words as stepping the reference's stream (rng.cpp:23-45) one draw
-    at a time: chunk jumps of 34 * 256 draws and the random-start jump of 2^(S+1) draws."""
-    skip = (2 << init_spins if init_spins >= 0 else 0) + chunks * 34 * 256 + extra
+    at a time: chunk jumps of 34 * tg_rng_chunk_steps() draws and the random-start jump of
+    2^(S+1) draws."""
+    skip = (2 << init_spins if init_spins >= 0 else 0) + chunks * 34 * int(tg.lib().tg_rng_chunk_steps()) + extra
     want = oracle.first_u64(seed, p, skip + 8)[skip:]
     got = tg.rng_jump_words(seed, p, chunks, extra, 8, init_spins)
     assert np.array_equal(got, want)

@@ -56,7 +56,7 @@ def test_t2_t3_gate_stream(oracle, spins, initial):
     (5, 3, 300, True, (1 << 63) + 5),  # forced rejections after random-start draws
 ])
 def test_t2_rng_chunked_jump_ahead(spins, rows, steps, random_init, reject_below):
-    """The pre-pass's chunked xoshiro256++ (chunks of 256 steps started by GF(2) jump
+    """The pre-pass's chunked xoshiro256++ (chunks of 64 steps started by GF(2) jump
     matrices, rejection fixup) reproduces one sequential stream per replica word for word."""
     assert tg.probe_rng_chunking(spins, rows, steps, random_init, reject_below) == 0
 
