@@ -2,86 +2,161 @@
 // batcher (VirtualDevice::batched_gemm, exec.cpp:144-221; per-entry math linalg.cpp:79-113:
 // out = alpha*A*B + beta*C, column-major interleaved complex128).
 //
-// grid = (tiles_m * tiles_n, batch); each CTA computes one 64x64 output tile of one batch
-// entry with 8 warps (16x32 sub-tile each, 2x4 blocks). K streams in chunks of 32 through
-// SMEM, de-interleaved into planar Re/Im tiles (A as [k][i], B transposed as [k][j], pitch
-// 68 doubles: conflict-free fragments). Complex product by real split:
-//   Re = Ar Br - Ai Bi,  Im = Ar Bi + Ai Br   (4 DMMA per block per k-chunk of 4).
-// Edges (m, n, k not multiples of the tile) are zero-padded in SMEM.
+// Persistent: one CTA of 8 warps per SM walks the work items (entry e, 64x64 output tile)
+// w = blockIdx.x, blockIdx.x + gridDim.x, ...; each warp owns a 16x32 sub-tile (2x4 blocks
+// of 8x8). K streams in chunks of 32 through a 3-stage cp.async pipeline that runs on
+// across work items (the next item's first chunks load during the current item's last
+// ones), the HBM tier's scheme (hbm_tier.cuh). Operands stay interleaved complex in SMEM
+// (cp.async copies one 16-byte element, no de-interleave pass): A as [k][i] with pitch 66
+// elements, B as [j][k] with pitch 36; a fragment is one LDS.128 (re, im), and the pitches
+// (2 and 4 mod 8 elements) make every quarter-warp of 8 such loads bank-conflict free.
+// Complex product by real split: Re = Ar Br - Ai Bi, Im = Ar Bi + Ai Br (4 DMMA per block
+// per k-step of 4). Edges (m, n, k not multiples of the tile) are zero-filled by the copy.
+#include <algorithm>
+
 #include "smem_tier.cuh"
 #include "tg_internal.h"
 
 namespace tg {
 namespace {
 
-constexpr int ZT = 64, ZK = 32, ZP = ZT + 4;
-constexpr int ZThreads = 256;
+constexpr int ZT = 64, ZK = 32;
+constexpr int PA = ZT + 2;  // A stage [k][i]: pitch 66 elements (16 B each)
+constexpr int PB = ZK + 4;  // B stage [j][k]: pitch 36
+constexpr int ZThreads = 256, ZStages = 3;
+constexpr int StageA = ZK * PA, StageB = ZT * PB;  // elements
+constexpr int StageElems = StageA + StageB;
 
-__global__ void __launch_bounds__(ZThreads, 1)
-    zgemm_kernel(int m, int n, int k, double ar, double ai, const double* __restrict__ A,
-                 int64_t sA, const double* __restrict__ B, int64_t sB, double br, double bi,
-                 const double* __restrict__ C, int64_t sC, double* __restrict__ out, int64_t sO,
-                 int fault) {
-  extern __shared__ __align__(16) double zsm[];
-  double *sAr = zsm, *sAi = zsm + ZK * ZP, *sBr = zsm + 2 * ZK * ZP, *sBi = zsm + 3 * ZK * ZP;
-  const int tiles_n = (n + ZT - 1) / ZT;
-  const int i0 = (blockIdx.x / tiles_n) * ZT, j0 = (blockIdx.x % tiles_n) * ZT;
-  const size_t e = blockIdx.y;
-  const double* a = A + 2 * sA * e;
-  const double* b = B + 2 * sB * e;
+__device__ __forceinline__ void cp_async16_zfill(void* s, const void* g, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(s)), "l"(g), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+struct ZArgs {
+  int m, n, k, tm, tn, nk;
+  double ar, ai, br, bi;
+  const double* A;
+  int64_t sA;
+  const double* B;
+  int64_t sB;
+  const double* C;
+  int64_t sC;
+  double* out;
+  int64_t sO;
+  int fault;
+  int64_t items;
+};
+
+__global__ void __launch_bounds__(ZThreads, 1) zgemm_kernel(const ZArgs P) {
+  extern __shared__ __align__(16) double2 zsm[];  // ZStages x {A [k][i], B [j][k]}
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wr = warp >> 1, wc = warp & 1;  // warp grid 4 x 2
   const int mm = lane >> 2, kq = lane & 3;
+  const int64_t mine = P.items > blockIdx.x ? (P.items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t total = mine * P.nk;
+  // Work-item cursors (the producer runs two chunks ahead of the consumer): item w -> entry
+  // e = w / (tm*tn), tile t = w % (tm*tn); decomposed once per item, never per chunk (64-bit
+  // divisions per chunk would sit on every warp's issue path between the DMMA phases).
+  struct Cursor {
+    int64_t w;
+    int kc, i0, j0;
+    const double *a, *b;
+  };
+  auto set_item = [&](Cursor& q, int64_t w) {
+    q.w = w;
+    q.kc = 0;
+    if (w < P.items) {
+      const int64_t e = w / (P.tm * P.tn);
+      const int t = static_cast<int>(w - e * P.tm * P.tn);
+      q.i0 = (t / P.tn) * ZT;
+      q.j0 = (t % P.tn) * ZT;
+      q.a = P.A + 2 * P.sA * e;
+      q.b = P.B + 2 * P.sB * e;
+    }
+  };
+  auto advance = [&](Cursor& q) {
+    if (++q.kc == P.nk) set_item(q, q.w + gridDim.x);
+  };
+  Cursor prod, cons;
+  set_item(prod, blockIdx.x);
+  set_item(cons, blockIdx.x);
+  int pslot = 0, cslot = 0;  // stage slots (it % ZStages) of producer and consumer, in 32 bits
+  // Stage copies of the producer's (item, chunk): thread tid copies A elements
+  // (i0 + ii, k0 + kk0 + 4u) and B elements (k0 + kb, j0 + jb0 + 8u), u = 0..7 (coalesced:
+  // consecutive threads take consecutive rows of one column). Addresses are set up once per
+  // chunk; in the main loop the 16 copies are spread 2 per k-step.
+  const int ii = tid & (ZT - 1), kk0 = tid >> 6;   // A
+  const int kb_ = tid & (ZK - 1), jb0 = tid >> 5;  // B
+  struct Stage {
+    const double *a, *b;
+    int64_t astep, bstep;
+    double2* st;
+    bool arow_ok, bk_ok;
+    int k0, j0;
+  } ps{};
+  auto prepare = [&]() {  // the producer's next stage
+    ps.k0 = prod.kc * ZK;
+    ps.j0 = prod.j0;
+    const int gi = prod.i0 + ii, gka = ps.k0 + kk0, gkb = ps.k0 + kb_;
+    ps.arow_ok = gi < P.m;
+    ps.bk_ok = gkb < P.k;
+    ps.a = prod.a + 2 * (static_cast<int64_t>(gi) + static_cast<int64_t>(gka) * P.m);
+    ps.b = prod.b + 2 * (static_cast<int64_t>(gkb) + static_cast<int64_t>(prod.j0 + jb0) * P.k);
+    ps.astep = 2 * 4 * static_cast<int64_t>(P.m);
+    ps.bstep = 2 * 8 * static_cast<int64_t>(P.k);
+    ps.st = zsm + pslot * StageElems;
+  };
+  auto copy_part = [&](int u) {  // copies u of the prepared stage
+    const bool oka = ps.arow_ok && ps.k0 + kk0 + 4 * u < P.k;
+    const bool okb = ps.bk_ok && ps.j0 + jb0 + 8 * u < P.n;
+    cp_async16_zfill(ps.st + (kk0 + 4 * u) * PA + ii, oka ? ps.a + u * ps.astep : P.A, oka);
+    cp_async16_zfill(ps.st + StageA + (jb0 + 8 * u) * PB + kb_, okb ? ps.b + u * ps.bstep : P.B, okb);
+  };
+  auto finish = [&]() {
+    advance(prod);
+    pslot = pslot == ZStages - 1 ? 0 : pslot + 1;
+  };
+  auto issue_all = [&](int64_t it) {  // prologue: a whole stage at once
+    if (it < total) {
+      prepare();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) copy_part(u);
+      finish();
+    }
+    cp_async_commit();
+  };
   double cr[2][4][2], ci[2][4][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-
-  for (int k0 = 0; k0 < k; k0 += ZK) {
-    // A tile: rows i0..i0+63, cols k0..k0+31 -> sA*[kk][ii]
-    for (int c = tid; c < ZT * ZK; c += ZThreads) {
-      const int ii = c % ZT, kk = c / ZT;
-      const int gi = i0 + ii, gk = k0 + kk;
-      double vr = 0.0, vi = 0.0;
-      if (gi < m && gk < k) {
-        const double2 v = *reinterpret_cast<const double2*>(a + 2 * (gi + static_cast<size_t>(gk) * m));
-        vr = v.x;
-        vi = v.y;
-      }
-      sAr[kk * ZP + ii] = vr;
-      sAi[kk * ZP + ii] = vi;
-    }
-    // B tile: rows k0..k0+31, cols j0..j0+63 -> sB*[kk][jj]
-    for (int c = tid; c < ZT * ZK; c += ZThreads) {
-      const int kk = c % ZK, jj = c / ZK;
-      const int gk = k0 + kk, gj = j0 + jj;
-      double vr = 0.0, vi = 0.0;
-      if (gk < k && gj < n) {
-        const double2 v = *reinterpret_cast<const double2*>(b + 2 * (gk + static_cast<size_t>(gj) * k));
-        vr = v.x;
-        vi = v.y;
-      }
-      sBr[kk * ZP + jj] = vr;
-      sBi[kk * ZP + jj] = vi;
-    }
-    __syncthreads();
+  issue_all(0);
+  issue_all(1);
+  for (int64_t it = 0; it < total; ++it) {
+    cp_async_wait<1>();          // this thread's copies of stage `it` landed
+    __syncthreads();             // everyone's did; stage (it-1) % 3 is free
+    const bool has_next = it + 2 < total;
+    if (has_next) prepare();
+    const double2* st = zsm + cslot * StageElems;
+    cslot = cslot == ZStages - 1 ? 0 : cslot + 1;
+    const double2* sa = st;
+    const double2* sb = st + StageA;
 #pragma unroll
     for (int kb = 0; kb < ZK; kb += 4) {
-      const int col = (kb + kq) * ZP;
+      if (has_next) copy_part(kb / 4);
       double xa[2], ya[2], yn[2], xb[4], yb[4];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int row = (wr * 2 + i) * 8 + mm;
-        xa[i] = sAr[row + col];
-        ya[i] = sAi[row + col];
-        yn[i] = -ya[i];
+        const double2 v = sa[(kb + kq) * PA + (wr * 2 + i) * 8 + mm];
+        xa[i] = v.x;
+        ya[i] = v.y;
+        yn[i] = -v.y;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int cc = (wc * 4 + j) * 8 + mm;
-        xb[j] = sBr[cc + col];
-        yb[j] = sBi[cc + col];
+        const double2 v = sb[((wc * 4 + j) * 8 + mm) * PB + kb + kq];
+        xb[j] = v.x;
+        yb[j] = v.y;
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i)
@@ -93,44 +168,55 @@ __global__ void __launch_bounds__(ZThreads, 1)
           dmma(ci[i][j][0], ci[i][j][1], ya[i], xb[j]);
         }
     }
-    __syncthreads();
-  }
-  // fault hook (linalg.cpp:94): sign of the first term of element (0,0) flipped
-  if (fault && i0 == 0 && j0 == 0 && wr == 0 && wc == 0 && lane == 0) {
-    const double2 a00 = *reinterpret_cast<const double2*>(a);
-    const double2 b00 = *reinterpret_cast<const double2*>(b);
-    const double tr = __dsub_rn(__dmul_rn(a00.x, b00.x), __dmul_rn(a00.y, b00.y));
-    cr[0][0][0] -= 2.0 * tr;
-  }
-  // epilogue (linalg.cpp:98-101): out = alpha*sum + beta*C, reference operation order
-  const double* c = C ? C + 2 * sC * e : nullptr;
-  double* o = out + 2 * sO * e;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int gi = i0 + (wr * 2 + i) * 8 + mm;
-        const int gj = j0 + (wc * 4 + j) * 8 + 2 * kq + h;
-        if (gi < m && gj < n) {
-          const size_t idx = gi + static_cast<size_t>(gj) * m;
-          double cvr = 0.0, cvi = 0.0;
-          if (c) {
-            const double2 v = *reinterpret_cast<const double2*>(c + 2 * idx);
-            cvr = v.x;
-            cvi = v.y;
-          }
-          const double sr = cr[i][j][h], si = ci[i][j][h];
-          const double re = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(ar, sr), __dmul_rn(ai, si)),
-                                                __dmul_rn(br, cvr)),
-                                      __dmul_rn(bi, cvi));
-          const double im = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(ar, si), __dmul_rn(ai, sr)),
-                                                __dmul_rn(br, cvi)),
-                                      __dmul_rn(bi, cvr));
-          *reinterpret_cast<double2*>(o + 2 * idx) = make_double2(re, im);
-        }
+    if (has_next) finish();
+    cp_async_commit();
+    if (cons.kc == P.nk - 1) {  // item epilogue
+      const int64_t e = cons.w / (P.tm * P.tn);
+      const int i0 = cons.i0, j0 = cons.j0;
+      const double* a = cons.a;
+      const double* b = cons.b;
+      // fault hook (linalg.cpp:94): sign of the first term of element (0,0) flipped
+      if (P.fault && i0 == 0 && j0 == 0 && wr == 0 && wc == 0 && lane == 0) {
+        const double2 a00 = *reinterpret_cast<const double2*>(a);
+        const double2 b00 = *reinterpret_cast<const double2*>(b);
+        const double tr = __dsub_rn(__dmul_rn(a00.x, b00.x), __dmul_rn(a00.y, b00.y));
+        cr[0][0][0] -= 2.0 * tr;
       }
+      // out = alpha*sum + beta*C (linalg.cpp:98-101), reference operation order
+      const double* c = P.C ? P.C + 2 * P.sC * e : nullptr;
+      double* o = P.out + 2 * P.sO * e;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gi = i0 + (wr * 2 + i) * 8 + mm;
+            const int gj = j0 + (wc * 4 + j) * 8 + 2 * kq + h;
+            if (gi < P.m && gj < P.n) {
+              const size_t idx = gi + static_cast<size_t>(gj) * P.m;
+              double cvr = 0.0, cvi = 0.0;
+              if (c) {
+                const double2 v = *reinterpret_cast<const double2*>(c + 2 * idx);
+                cvr = v.x;
+                cvi = v.y;
+              }
+              const double sr = cr[i][j][h], si = ci[i][j][h];
+              const double re = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(P.ar, sr), __dmul_rn(P.ai, si)),
+                                                    __dmul_rn(P.br, cvr)),
+                                          __dmul_rn(P.bi, cvi));
+              const double im = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(P.ar, si), __dmul_rn(P.ai, sr)),
+                                                    __dmul_rn(P.br, cvi)),
+                                          __dmul_rn(P.bi, cvr));
+              *reinterpret_cast<double2*>(o + 2 * idx) = make_double2(re, im);
+            }
+            cr[i][j][h] = 0.0;
+            ci[i][j][h] = 0.0;
+          }
+    }
+    advance(cons);
+  }
+  cp_async_wait<0>();
 }
 
 }  // namespace
@@ -140,13 +226,35 @@ cudaError_t launch_zgemm_strided(int batch, int m, int n, int k, double ar, doub
                                  double br, double bi, const double* C, int64_t sC, double* out,
                                  int64_t sO, int inject_fault, cudaStream_t stream) {
   if (batch < 1 || m < 1 || n < 1 || k < 1) return cudaErrorInvalidValue;
-  const int tiles = ((m + ZT - 1) / ZT) * ((n + ZT - 1) / ZT);
-  dim3 grid(tiles, batch);
-  constexpr int bytes = 4 * ZK * ZP * 8;
+  ZArgs P{};
+  P.m = m;
+  P.n = n;
+  P.k = k;
+  P.tm = (m + ZT - 1) / ZT;
+  P.tn = (n + ZT - 1) / ZT;
+  P.nk = (k + ZK - 1) / ZK;
+  P.ar = ar;
+  P.ai = ai;
+  P.br = br;
+  P.bi = bi;
+  P.A = A;
+  P.sA = sA;
+  P.B = B;
+  P.sB = sB;
+  P.C = C;
+  P.sC = sC;
+  P.out = out;
+  P.sO = sO;
+  P.fault = inject_fault;
+  P.items = static_cast<int64_t>(batch) * P.tm * P.tn;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  constexpr int bytes = ZStages * StageElems * 16;
   cudaError_t e = cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
-  zgemm_kernel<<<grid, ZThreads, bytes, stream>>>(m, n, k, ar, ai, A, sA, B, sB, br, bi, C, sC, out,
-                                              sO, inject_fault);
+  const int grid = static_cast<int>(std::min<int64_t>(P.items, sms));
+  zgemm_kernel<<<grid, ZThreads, bytes, stream>>>(P);
   return cudaGetLastError();
 }
 
