@@ -12,3 +12,17 @@ with tg.Device([0]) as d:
                                       (13, 3, 1, "von-neumann"), (10, 3, 1, "von-neumann")):
         r = d.run(tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=1, entropy_kind=kind))
         print(spins, kind, int(r.accepted.sum()))
+
+# the batched-GEMM kernel, with ragged edges (zero-filled copies) and a C operand
+import numpy as np  # noqa: E402
+
+rng = np.random.default_rng(0)
+with tg.Device([0]) as d:
+    for m, n, k, nb in ((70, 33, 45, 3), (64, 64, 64, 2), (5, 130, 7, 2)):
+        A = [rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k)) for _ in range(nb)]
+        B = [rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n)) for _ in range(nb)]
+        Cm = [rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n)) for _ in range(nb)]
+        out = d.batched_gemm(A, B, Cm, alpha=0.5 - 1j, beta=2.0)
+        err = max(np.abs(o - ((0.5 - 1j) * a @ b + 2.0 * c)).max() for o, a, b, c in zip(out, A, B, Cm))
+        print("zgemm", m, n, k, nb, f"{err:.1e}")
+        assert err < 1e-9
