@@ -487,6 +487,14 @@ size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int
   return static_cast<size_t>(clusters) * (4 * (size_t{1} << spins) + rho) * sizeof(double);
 }
 
+uint64_t anneal_hbm_wave_rows(const AnnealParams& p) {  // co-resident clusters = replicas per wave
+  int dev = 0, cs = 1;
+  uint64_t clusters = 0;
+  cudaGetDevice(&dev);
+  if (hbm_geometry(p.spins, p.rows, p.entropy_kind, dev, cs, clusters) != cudaSuccess) return 0;
+  return clusters;
+}
+
 cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out,
                               bool trace) {
   if (p.spins < 13 || p.spins > 24) return cudaErrorInvalidValue;

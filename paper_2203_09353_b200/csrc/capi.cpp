@@ -45,7 +45,8 @@ tg_status cuda_fail(cudaError_t e, const char* where) {
 struct DeviceState {
   int ordinal = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t copy = nullptr;  // trace copy-back of finished waves, overlapping the last wave
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_part = nullptr;
   // grow-only device buffers reused across calls
   void* trace = nullptr;
   size_t trace_bytes = 0;
@@ -227,8 +228,10 @@ tg_status tg_create(const int* gpus, int n, tg_ctx** out) {
                                   std::to_string(count) + " visible)");
     TG_CUDA(cudaSetDevice(d.ordinal));
     TG_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    TG_CUDA(cudaStreamCreateWithFlags(&d.copy, cudaStreamNonBlocking));
     TG_CUDA(cudaEventCreate(&d.ev0));
     TG_CUDA(cudaEventCreate(&d.ev1));
+    TG_CUDA(cudaEventCreateWithFlags(&d.ev_part, cudaEventDisableTiming));
     ctx->devs.push_back(d);
   }
   *out = ctx.release();
@@ -249,9 +252,12 @@ tg_status tg_destroy(tg_ctx* ctx) {
     cudaStreamSynchronize(d.stream);
     if (d.trace) cudaFree(d.trace);
     if (d.workspace) cudaFree(d.workspace);
+    cudaStreamSynchronize(d.copy);
     cudaEventDestroy(d.ev0);
     cudaEventDestroy(d.ev1);
+    cudaEventDestroy(d.ev_part);
     cudaStreamDestroy(d.stream);
+    cudaStreamDestroy(d.copy);
   }
   delete ctx;
   return TG_OK;
@@ -354,30 +360,70 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
       if (!cu(cudaMalloc(&d.workspace, ws), "cudaMalloc(workspace)")) return;
       d.workspace_bytes = ws;
     }
-    if (!cu(cudaEventRecord(d.ev0, d.stream), "cudaEventRecord")) return;
-    if (!cu(launch(p, d.workspace, d.workspace_bytes, d.stream), "anneal launch")) return;
-    if (!cu(cudaEventRecord(d.ev1, d.stream), "cudaEventRecord")) return;
-    // copy back: rows of this GPU are host rows g + D*q
-    std::vector<double> init(lrows), fin(lrows), ent(lrows * steps);
-    std::vector<uint8_t> acc(lrows * steps), sit(want_sites ? lrows * steps : 0);
-    std::vector<int64_t> wall(want_wall ? lrows * steps : 0);
+    // Replicas run in waves of `wave` (resident CTAs / clusters). With D == 1 the traces go
+    // straight into the caller's arrays, so the rows of all full waves but the last are
+    // launched first and copied back on a second stream while the remaining rows run.
+    uint64_t split = 0;
+    if (D == 1 && steps > 0) {
+      const uint64_t wave = p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::anneal_smem_wave_rows(p)
+                                                                                : tg::anneal_hbm_wave_rows(p);
+      if (wave > 0 && lrows > wave) split = lrows % wave ? lrows - lrows % wave : lrows - wave;
+    }
+    auto rows_of = [&](uint64_t r0, uint64_t r1) {  // AnnealParams of host rows [r0, r1)
+      tg::AnnealParams q = p;
+      q.rows = r1 - r0;
+      q.p_first = p.p_first + r0 * p.p_stride;
+      q.initial_entropy = p.initial_entropy + r0;
+      q.final_entropy = p.final_entropy + r0;
+      q.status = p.status + r0;
+      q.status_step = p.status_step + r0;
+      q.entropies = p.entropies + r0 * steps;
+      q.accepted = p.accepted + r0 * steps;
+      q.sites = p.sites ? p.sites + r0 * steps : nullptr;
+      q.wall_ns = p.wall_ns ? p.wall_ns + r0 * steps : nullptr;
+      return q;
+    };
+    std::vector<double> init(lrows), fin(lrows), ent(D > 1 ? lrows * steps : 0);
+    std::vector<uint8_t> acc(D > 1 ? lrows * steps : 0), sit(want_sites && D > 1 ? lrows * steps : 0);
+    std::vector<int64_t> wall(want_wall && D > 1 ? lrows * steps : 0);
     status[g].resize(lrows);
     status_step[g].resize(lrows);
-    bool ok = cu(cudaMemcpyAsync(init.data(), p.initial_entropy, 8 * lrows, cudaMemcpyDeviceToHost, d.stream), "D2H") &&
-              cu(cudaMemcpyAsync(fin.data(), p.final_entropy, 8 * lrows, cudaMemcpyDeviceToHost, d.stream), "D2H") &&
-              cu(cudaMemcpyAsync(status[g].data(), p.status, 4 * lrows, cudaMemcpyDeviceToHost, d.stream), "D2H") &&
-              cu(cudaMemcpyAsync(status_step[g].data(), p.status_step, 8 * lrows, cudaMemcpyDeviceToHost, d.stream), "D2H");
-    if (ok && steps > 0) {
-      // D == 1 and host rows contiguous: copy straight into the caller's arrays
-      double* ent_dst = D == 1 ? res->entropies : ent.data();
-      uint8_t* acc_dst = D == 1 ? res->accepted : acc.data();
-      ok = cu(cudaMemcpyAsync(ent_dst, p.entropies, 8 * lrows * steps, cudaMemcpyDeviceToHost, d.stream), "D2H") &&
-           cu(cudaMemcpyAsync(acc_dst, p.accepted, lrows * steps, cudaMemcpyDeviceToHost, d.stream), "D2H");
-      if (ok && want_sites)
-        ok = cu(cudaMemcpyAsync(D == 1 ? res->sites : sit.data(), p.sites, lrows * steps, cudaMemcpyDeviceToHost, d.stream), "D2H");
-      if (ok && want_wall)
-        ok = cu(cudaMemcpyAsync(D == 1 ? res->wall_ns : wall.data(), p.wall_ns, 8 * lrows * steps, cudaMemcpyDeviceToHost, d.stream), "D2H");
+    // trace rows [r0, r1) -> host (caller arrays when D == 1) on stream `st`
+    auto copy_back = [&](uint64_t r0, uint64_t r1, cudaStream_t st) {
+      const uint64_t n = r1 - r0, o = r0 * steps, ns = n * steps;
+      bool ok = cu(cudaMemcpyAsync(init.data() + r0, p.initial_entropy + r0, 8 * n, cudaMemcpyDeviceToHost, st), "D2H") &&
+                cu(cudaMemcpyAsync(fin.data() + r0, p.final_entropy + r0, 8 * n, cudaMemcpyDeviceToHost, st), "D2H") &&
+                cu(cudaMemcpyAsync(status[g].data() + r0, p.status + r0, 4 * n, cudaMemcpyDeviceToHost, st), "D2H") &&
+                cu(cudaMemcpyAsync(status_step[g].data() + r0, p.status_step + r0, 8 * n, cudaMemcpyDeviceToHost, st), "D2H");
+      if (ok && steps > 0) {
+        // D == 1 and host rows contiguous: copy straight into the caller's arrays
+        double* ent_dst = D == 1 ? res->entropies + o : ent.data() + o;
+        uint8_t* acc_dst = D == 1 ? res->accepted + o : acc.data() + o;
+        ok = cu(cudaMemcpyAsync(ent_dst, p.entropies + o, 8 * ns, cudaMemcpyDeviceToHost, st), "D2H") &&
+             cu(cudaMemcpyAsync(acc_dst, p.accepted + o, ns, cudaMemcpyDeviceToHost, st), "D2H");
+        if (ok && want_sites)
+          ok = cu(cudaMemcpyAsync(D == 1 ? res->sites + o : sit.data() + o, p.sites + o, ns, cudaMemcpyDeviceToHost, st), "D2H");
+        if (ok && want_wall)
+          ok = cu(cudaMemcpyAsync(D == 1 ? res->wall_ns + o : wall.data() + o, p.wall_ns + o, 8 * ns,
+                                  cudaMemcpyDeviceToHost, st), "D2H");
+      }
+      return ok;
+    };
+    if (!cu(cudaEventRecord(d.ev0, d.stream), "cudaEventRecord")) return;
+    bool ok = true;
+    if (split > 0) {
+      if (!cu(launch(rows_of(0, split), d.workspace, d.workspace_bytes, d.stream), "anneal launch")) return;
+      if (!cu(cudaEventRecord(d.ev_part, d.stream), "cudaEventRecord")) return;
+      if (!cu(cudaStreamWaitEvent(d.copy, d.ev_part, 0), "cudaStreamWaitEvent")) return;
+      ok = copy_back(0, split, d.copy);
+      if (!ok) return;
+      if (!cu(launch(rows_of(split, lrows), d.workspace, d.workspace_bytes, d.stream), "anneal launch")) return;
+    } else {
+      if (!cu(launch(p, d.workspace, d.workspace_bytes, d.stream), "anneal launch")) return;
     }
+    if (!cu(cudaEventRecord(d.ev1, d.stream), "cudaEventRecord")) return;
+    ok = copy_back(split, lrows, d.stream);
+    if (ok && split > 0) ok = cu(cudaStreamSynchronize(d.copy), "trace copy");
     if (!ok) return;
     if (!cu(cudaStreamSynchronize(d.stream), "anneal kernel")) return;
     cudaEventElapsedTime(&ms[g], d.ev0, d.ev1);

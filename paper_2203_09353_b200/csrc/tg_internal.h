@@ -55,6 +55,9 @@ constexpr int kSmemMaxSpins = 12;
 constexpr int kVnMaxSpins = 15;  // device von Neumann: d_a <= 64 (vn.cuh: SMEM tier, HBM tier S=13), d_a = 128 (vn_packed.cuh: S=14,15)
 
 // anneal_smem.cu (S <= 12)
+// replicas processed per wave by one launch (resident CTAs / clusters), 0 if unknown
+uint64_t anneal_smem_wave_rows(const AnnealParams& p);
+uint64_t anneal_hbm_wave_rows(const AnnealParams& p);
 cudaError_t launch_anneal_smem(const AnnealParams& p, cudaStream_t stream, int* grid_out,
                                bool trace = false);
 // anneal_hbm.cu (S >= 13)
