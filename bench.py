@@ -42,8 +42,9 @@ UNIT = "replica-steps/s"
 CONFIGS = {  # BASELINE.json configs (per GPU for the weak-scaling multi-GPU runs)
     1: dict(spins=8, replicas=64, mc_steps=1000, name="config1: L=8, 64 replicas, 1000 MC steps"),
     2: dict(spins=12, replicas=1024, mc_steps=10000, name="config2: L=12, 1024 replicas/GPU, 10000 MC steps"),
-    3: dict(spins=16, replicas=4096, mc_steps=20, name="config3: L=16 (256x256 GEMMs), 4096 replicas/GPU"),
-    4: dict(spins=20, replicas=512, mc_steps=2, name="config4: L=20 (1024x1024 GEMMs), 512 replicas/GPU"),
+    # configs 3/4: BASELINE.json leaves the step count open; SURVEY.md §8(d) fixes 1000 / 100
+    3: dict(spins=16, replicas=4096, mc_steps=1000, name="config3: L=16 (256x256 GEMMs), 4096 replicas/GPU, 1000 MC steps"),
+    4: dict(spins=20, replicas=512, mc_steps=100, name="config4: L=20 (1024x1024 GEMMs), 512 replicas/GPU, 100 MC steps"),
     5: dict(spins=14, replicas=65536, mc_steps=100, name="config5: L=14, 65536 replicas/GPU, 100 MC steps"),
 }
 
