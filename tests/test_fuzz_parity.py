@@ -1,0 +1,48 @@
+"""Randomised parity sweep: device trajectories against the oracle over random chain
+lengths (both tiers, every CTA-per-replica geometry), replica counts, step counts that cross
+the pre-pass's chunk boundaries and the renormalisation interval, objectives, initial states
+and entropy kinds. Sites and accept flags bit-exact, entropies within 1e-10 (scaled)."""
+import numpy as np
+import pytest
+from oracle_lib import McCfg
+
+import paper_2203_09353_b200 as tg
+
+TOL = 1e-10
+
+
+def cases(n=120, seed=2025):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        spins = int(rng.choice([2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 12, 12, 13, 14, 14, 15, 16]))
+        vn = spins <= 12 and rng.random() < 0.3
+        steps = int(rng.choice([1, 3, 17, 64, 65, 130, 257])) if spins <= 12 else int(rng.choice([1, 5, 9]))
+        procs = int(rng.choice([1, 2, 3, 7])) if spins >= 14 else int(rng.choice([1, 2, 5, 13]))
+        renorm = int(rng.choice([0, 7, 1000]))
+        out.append(dict(spins=spins, steps=steps, procs=procs, seed=int(rng.integers(0, 1 << 31)),
+                        objective=int(rng.integers(0, 2)), initial=int(rng.integers(0, 2)),
+                        kind=0 if vn else 1, renorm=renorm))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("c", cases(), ids=lambda c: "S{spins}-n{procs}x{steps}-k{kind}-o{objective}-i{initial}-r{renorm}".format(**c))
+def test_fuzz_trajectory_parity(device, oracle, c):
+    cfg = tg.ExperimentConfig(spins=c["spins"], steps=c["steps"], procedures=c["procs"], seed=c["seed"],
+                              objective="max" if c["objective"] == 0 else "min",
+                              initial_state="product" if c["initial"] == 0 else "random",
+                              entropy_kind="renyi-2" if c["kind"] == 1 else "von-neumann",
+                              renormalize_interval=c["renorm"])
+    rep = device.run(cfg)
+    want = oracle.run(McCfg(spins=c["spins"], steps=c["steps"], seed=c["seed"], entropy_kind=c["kind"],
+                            objective=c["objective"], initial_state=c["initial"], renormalize_interval=c["renorm"]),
+                      0, c["procs"])
+    assert np.array_equal(rep.sites, want.sites)
+    mism = np.argwhere(rep.accepted != want.accepted)
+    assert mism.size == 0, f"accept flags differ at {mism[:5].tolist()}"
+    d = np.abs(rep.entropies - want.entropies) / np.maximum(np.abs(want.entropies), 1.0)
+    assert d.size == 0 or d.max() <= TOL, d.max()
+    d0 = np.abs(rep.initial_entropy - want.initial) / np.maximum(np.abs(want.initial), 1.0)
+    assert d0.max() <= TOL
