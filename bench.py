@@ -311,7 +311,7 @@ def main():
     d2h = rows * S * (8 + 1 + 1) + rows * (8 + 8 + 4 + 8)
 
     cpu_baseline = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the CPU sample: rank 0 at N=1 only
         cpu_baseline, _ = cpu_reference_sample(spins, R, S, os.cpu_count() or 1,
                                                entropy_kind=0 if args.entropy == "von-neumann" else 1)
 
