@@ -382,3 +382,22 @@ def test_hbm_cluster_split_bitwise(device, oracle, spins, procs, steps, monkeypa
     want = oracle.run(McCfg(spins=spins, steps=steps, seed=8, initial_state=1), 0, procs)
     assert np.array_equal(b.accepted, want.accepted)
     assert close(b.entropies, want.entropies).all()
+
+
+@pytest.mark.parametrize("spins,procs,steps", [(12, 7, 40), (14, 5, 6), (8, 9, 300)])
+def test_multi_device_binding_same_gpu(oracle, spins, procs, steps):
+    """The in-process multi-GPU path (one host thread + stream + buffers per device, replica
+    p on device p mod devices, bench.cpp:171) with both "devices" mapped to GPU 0: traces are
+    bitwise those of the one-device run, and match the oracle."""
+    cfg1 = tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=21, devices=1)
+    cfg2 = tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=21, devices=2)
+    with tg.Device([0]) as d1:
+        a = d1.run(cfg1)
+    with tg.Device([0, 0]) as d2:
+        b = d2.run(cfg2)
+    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
+    assert np.array_equal(a.accepted, b.accepted)
+    assert np.array_equal(a.sites, b.sites)
+    assert a.average_entropy == b.average_entropy
+    want = oracle.run(McCfg(spins=spins, steps=steps, seed=21), 0, procs)
+    assert np.array_equal(b.accepted, want.accepted)
