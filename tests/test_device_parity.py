@@ -401,3 +401,25 @@ def test_multi_device_binding_same_gpu(oracle, spins, procs, steps):
     assert a.average_entropy == b.average_entropy
     want = oracle.run(McCfg(spins=spins, steps=steps, seed=21), 0, procs)
     assert np.array_equal(b.accepted, want.accepted)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("spins", [22, 24])
+def test_largest_chains_invariants(monkeypatch, spins):
+    """S = 22 and 24 (2^24 amplitudes, 4096^3 complex GEMMs): too large for the oracle, so
+    the invariants — 1-CTA and 4-CTA runs bitwise equal, every state normalised (no kernel
+    error), entropies within [0, floor(S/2) ln 2], and a Haar-random start near Page's value."""
+    cfg = tg.ExperimentConfig(spins=spins, steps=2, procedures=1, seed=17, initial_state="random")
+    monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", "1")
+    with tg.Device([0]) as d:
+        a = d.run(cfg)
+    monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", "4")
+    with tg.Device([0]) as d:
+        b = d.run(cfg)
+    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
+    assert np.array_equal(a.initial_entropy.view(np.uint64), b.initial_entropy.view(np.uint64))
+    bound = (spins // 2) * math.log(2) + 1e-9
+    assert np.all(a.entropies >= 0) and np.all(a.entropies <= bound)
+    assert 0 <= a.initial_entropy[0] <= bound
+    # a Haar-random state of 2^S amplitudes is close to maximally entangled (Page)
+    assert a.initial_entropy[0] > bound - 1.5
