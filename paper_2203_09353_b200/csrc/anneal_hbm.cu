@@ -12,8 +12,12 @@
 // Every FP64 op outside the GEMM runs while no DMMA is in flight on the SM (the FP64 pipe
 // is shared, profiles/r01_fp64_contention.txt). The proposal stream comes from the
 // pre-pass (gate_stream.cu).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "hbm_tier.cuh"
 #include "tg_internal.h"
@@ -28,11 +32,15 @@ struct HHeader {
   double part[kWarps][2 * kChains];  // per-warp chain values {rho chain 0..3, tr chain 0..3}
   double val[kMaxCS][2 * kChains];   // per-rank chain sums (other ranks' arrive by DSMEM)
   double norm_q[4];                  // renormalisation: sums over the four quarters of psi
+  uint64_t full[kStages];            // TMA pipeline (rho_partials_tma)
+  uint64_t empty[kStages];
   int32_t decision;
   int32_t error;
 };
 constexpr int kHHeaderBytes = (static_cast<int>(sizeof(HHeader)) + 127) / 128 * 128;
-constexpr int kSmemBytes = kHHeaderBytes + kStages * kStage * 8;
+// + 1 KB: the anneal kernel aligns its stages to 1 KB (the TMA swizzle is a function of the
+// SMEM address bits)
+constexpr int kSmemBytes = kHHeaderBytes + kStages * kStage * 8 + 1024;
 // von Neumann (KIND 1, S = 13: d_a = 64 = one tile, CS = 1): rho planes (pitch 68) and the
 // solver scratch reuse the stage buffers once the GEMM pipeline has drained.
 constexpr int kRP = TB + 4;
@@ -109,18 +117,24 @@ __device__ void renormalize(const Geo& G, double* X, double* Y, int tid, int war
     __stcg(Y + i, __dmul_rn(__ldcg(Y + i), inv));
   }
   __threadfence();
+  fence_proxy_async_global();  // the next GEMM may read psi through the TMA engine
   sync_all<CS>();
 }
 
 // TRACE: phase stamps (clock64) of the first cluster's first replica into P.trace[steps][8]:
 // 0 step start, 1 gate pass done, 2 GEMM done, 3 decision done (profiling probe only).
 // KIND: 0 Renyi-2, 1 von Neumann (S = 13, CS = 1; vn.cuh after the GEMM).
-template <bool TRACE, int CS, int KIND>
-__global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealParams P) {
+// TMA (KIND 0): the GEMM stages are filled by the TMA engine from `tmap` (hbm_tensor_map,
+// rho_partials_tma) instead of per-thread cp.async.
+template <bool TRACE, int CS, int KIND, bool TMA>
+__global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealParams P,
+                                                                 const __grid_constant__ CUtensorMap tmap) {
   static_assert(KIND == 0 || CS == 1, "von Neumann runs one CTA per replica");
+  static_assert(KIND == 0 || !TMA, "the TMA pipeline is the Renyi-2 GEMM");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   HHeader& H = *reinterpret_cast<HHeader*>(smem_raw);
-  double* stages = reinterpret_cast<double*>(smem_raw + kHHeaderBytes);
+  const uint32_t sbase = smem_u32(smem_raw);
+  double* stages = reinterpret_cast<double*>(smem_raw + (((sbase + kHHeaderBytes + 1023u) & ~1023u) - sbase));
   double* Rr = stages;  // KIND 1 only (aliases the drained stages)
   double* Ri = stages + TB * kRP;
   vn::Scratch& VW = *reinterpret_cast<vn::Scratch*>(stages + 2 * TB * kRP);
@@ -151,12 +165,6 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
       return vn::entropy(Rr, Ri, TB, kRP, VW, threadIdx.x, [] { __syncthreads(); });
     }
   };
-  int64_t* gprof = nullptr;  // TRACE: GEMM-internal clocks of the current step (slots 4..6)
-  auto gemm = [&](const double* X, const double* Y, int first, int stride, double out[2 * kChains]) {
-    const int tid = threadIdx.x;
-    rho_partials<KIND == 1>(Geo(static_cast<int>(P.spins)), X, Y, stages, tid, tid >> 5, tid & 31, first,
-                            stride, P.inject_fault != 0, out, Rr, Ri, kRP, gprof, Rg);
-  };
   const Geo G(static_cast<int>(P.spins));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = CS == 1 ? 0u : cluster_rank();
@@ -165,6 +173,27 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
                                                          (packed ? 2 * static_cast<size_t>(G.da) * G.da : 0));
   auto PX = [&](int b) { return slab + (2 * b) * static_cast<size_t>(G.n); };
   auto PY = [&](int b) { return slab + (2 * b + 1) * static_cast<size_t>(G.n); };
+  TmaPipe pipe{H.full, H.empty, 0u};
+  if constexpr (TMA) {
+    if (tid == 0) {
+      for (int s = 0; s < kStages; ++s) {
+        mbar_init(&H.full[s], 1);
+        mbar_init(&H.empty[s], kWarps);
+      }
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
+  int64_t* gprof = nullptr;  // TRACE: GEMM-internal clocks of the current step (slots 4..6)
+  auto gemm = [&](int b, int first, int stride, double out[2 * kChains]) {  // rho of buffer b
+    if constexpr (TMA) {
+      rho_partials_tma(G, &tmap, b, static_cast<int>(cid), stages, pipe, tid, warp, lane, first, stride,
+                       P.inject_fault != 0, PX(b), PY(b), out, gprof);
+    } else {
+      rho_partials<KIND == 1>(G, PX(b), PY(b), stages, tid, warp, lane, first, stride, P.inject_fault != 0, out,
+                              Rr, Ri, kRP, gprof, Rg);
+    }
+  };
   auto mark = [&](uint64_t r, uint64_t s, int k) {
     if (TRACE && tid == 0 && rank == 0 && r == 0 && s < P.steps) P.trace[s * 8 + k] = clock64();
   };
@@ -190,13 +219,14 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
         }
       }
       __threadfence();
+      fence_proxy_async_global();
       sync_all<CS>();
     }
     int cur = 0;
     if (P.initial_state == 1) renormalize<CS>(G, PX(0), PY(0), tid, warp, lane, rank, H);
 
     double out[2 * kChains], rho2, tr;
-    gemm(PX(cur), PY(cur), first, stride, out);
+    gemm(cur, first, stride, out);
     if (lane == 0)
       for (int c = 0; c < 2 * kChains; ++c) H.part[warp][c] = out[c];
     publish_vals<CS>(H, tid, rank);
@@ -216,10 +246,11 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
       mark(r, s, 0);
       gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, kThreads);
       __threadfence();
+      if constexpr (TMA) fence_proxy_async_global();  // psi' is read by the TMA engine
       sync_all<CS>();
       mark(r, s, 1);
       if (TRACE && rank == 0 && r == 0 && s < P.steps) gprof = P.trace + s * 8 + 4;
-      gemm(PX(cur ^ 1), PY(cur ^ 1), first, stride, out);
+      gemm(cur ^ 1, first, stride, out);
       gprof = nullptr;
       if (lane == 0)
         for (int c = 0; c < 2 * kChains; ++c) H.part[warp][c] = out[c];
@@ -410,12 +441,64 @@ int ctas_per_replica(uint32_t spins, uint64_t rows, int sms, int entropy_kind) {
 
 namespace {
 
-using HbmKernel = void (*)(AnnealParams);
-HbmKernel hbm_kernel(int kind, int cs, bool trace) {
-  if (kind == 0) return trace ? hbm::anneal_hbm_kernel<true, 1, 1> : hbm::anneal_hbm_kernel<false, 1, 1>;
-  if (cs == 1) return trace ? hbm::anneal_hbm_kernel<true, 1, 0> : hbm::anneal_hbm_kernel<false, 1, 0>;
-  if (cs == 2) return trace ? hbm::anneal_hbm_kernel<true, 2, 0> : hbm::anneal_hbm_kernel<false, 2, 0>;
-  return trace ? hbm::anneal_hbm_kernel<true, 4, 0> : hbm::anneal_hbm_kernel<false, 4, 0>;
+using HbmKernel = void (*)(AnnealParams, CUtensorMap);
+template <bool TMA>
+HbmKernel hbm_kernel_renyi(int cs, bool trace) {
+  using namespace hbm;
+  if (cs == 1) return trace ? anneal_hbm_kernel<true, 1, 0, TMA> : anneal_hbm_kernel<false, 1, 0, TMA>;
+  if (cs == 2) return trace ? anneal_hbm_kernel<true, 2, 0, TMA> : anneal_hbm_kernel<false, 2, 0, TMA>;
+  return trace ? anneal_hbm_kernel<true, 4, 0, TMA> : anneal_hbm_kernel<false, 4, 0, TMA>;
+}
+
+// Renyi-2 GEMM stages through the TMA engine unless TG_HBM_TMA=0 (the cp.async pipeline).
+bool hbm_use_tma() {
+  static const bool on = [] {
+    const char* env = std::getenv("TG_HBM_TMA");
+    return !(env && env[0] == '0');
+  }();
+  return on;
+}
+
+HbmKernel hbm_kernel(int kind, int cs, bool trace, bool tma) {
+  if (kind == 0) return trace ? hbm::anneal_hbm_kernel<true, 1, 1, false> : hbm::anneal_hbm_kernel<false, 1, 1, false>;
+  return tma ? hbm_kernel_renyi<true>(cs, trace) : hbm_kernel_renyi<false>(cs, trace);
+}
+
+// The TMA view of the workspace (hbm_tier.cuh, rho_partials_tma): 5-D, FP64,
+//   dim0 8 rows (contiguous), dim1 column b (stride d_a), dim2 row block (stride 8 rows),
+//   dim3 plane 2 * buffer + {X, Y} (stride n), dim4 cluster slot (stride 4n),
+// box (8, KC, 8, 2, 1), 64-B swizzle. The encoder comes from the driver at run time (no
+// libcuda link dependency).
+using EncodeTiled = PFN_cuTensorMapEncodeTiled_v12000;
+EncodeTiled tensor_map_encoder() {
+  static const EncodeTiled fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiled>(nullptr);
+    return reinterpret_cast<EncodeTiled>(f);
+  }();
+  return fn;
+}
+
+cudaError_t hbm_tensor_map(const AnnealParams& p, uint64_t clusters, CUtensorMap* map) {
+  const EncodeTiled enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const uint64_t la = p.spins / 2, da = uint64_t{1} << la, db = uint64_t{1} << (p.spins - la);
+  const uint64_t n = uint64_t{1} << p.spins;
+  cuuint64_t dims[5] = {8, db, da / 8, 4, clusters};
+  cuuint64_t strides[4] = {da * 8, 64, n * 8, 4 * n * 8};
+  cuuint32_t box[5] = {8, static_cast<cuuint32_t>(hbm::KC), 8, 2, 1};
+  cuuint32_t elem[5] = {1, 1, 1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, p.workspace, dims, strides, box, elem,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    std::fprintf(stderr, "[tg] cuTensorMapEncodeTiled failed (%d)\n", static_cast<int>(r));
+    return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
 }
 
 cudaLaunchConfig_t hbm_config(int grid, int cs, cudaStream_t stream, cudaLaunchAttribute* attr) {
@@ -442,7 +525,7 @@ cudaError_t hbm_geometry(uint32_t spins, uint64_t rows, int kind, int device, in
   auto resident_for = [&](int c, int& resident) -> cudaError_t {
     resident = sms / c;
     if (c == 1) return cudaSuccess;
-    HbmKernel kern = hbm_kernel(kind, c, false);
+    HbmKernel kern = hbm_kernel(kind, c, false, false);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
     if (e != cudaSuccess) return e;
     cudaLaunchAttribute attr[1];
@@ -508,12 +591,19 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   const int grid = static_cast<int>(clusters) * cs;
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
-  HbmKernel kern = hbm_kernel(p.entropy_kind, cs, trace);
+  const bool tma = p.entropy_kind == 1 && hbm_use_tma();
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  if (tma) {
+    e = hbm_tensor_map(p, clusters, &tmap);
+    if (e != cudaSuccess) return e;
+  }
+  HbmKernel kern = hbm_kernel(p.entropy_kind, cs, trace, tma);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = hbm_config(grid, cs, stream, attr);
-  e = cudaLaunchKernelEx(&cfg, kern, p);
+  e = cudaLaunchKernelEx(&cfg, kern, p, tmap);
   if (e != cudaSuccess) return e;
   e = cudaGetLastError();
   if (e != cudaSuccess || p.entropy_kind == 0) return e;

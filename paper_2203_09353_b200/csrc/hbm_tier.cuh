@@ -169,6 +169,53 @@ __device__ __forceinline__ void load_stage(const double* X, const double* Y, int
   }
 }
 
+// Tile epilogue, part 1: the diagonal tile's trace into chain ch; the fault injection.
+__device__ __forceinline__ void tile_trace_fault(double (&cr)[2][4][2], double (&tr)[kChains], int ch, bool diag,
+                                                 bool fault, const double* X, const double* Y, int wr, int wc,
+                                                 int m, int kq, int lane) {
+  if (diag) {
+    double tsum = 0.0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) tsum = c == ch ? tr[c] : tsum;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (wr * 2 + i == wc * 4 + j) {
+          if (m == 2 * kq) tsum += cr[i][j][0];
+          if (m == 2 * kq + 1) tsum += cr[i][j][1];
+        }
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) tr[c] = c == ch ? tsum : tr[c];
+  }
+  if (fault && wr == 0 && wc == 0 && lane == 0) cr[0][0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);
+}
+
+// Tile epilogue, part 2: the tile's sum |rho_ij|^2 into chain ch, in four interleaved
+// sub-chains (the fold is 8 DFMA deep instead of 32: it runs next to other warps' DMMA
+// streams, which starve FP64 latency chains); zero the accumulators for the next tile.
+__device__ __forceinline__ void tile_fold(double (&cr)[2][4][2], double (&ci)[2][4][2], double (&rho)[kChains],
+                                          int ch, bool zero) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double& a = acc[((i * 4 + j) * 2 + e) & 3];
+        a = fma(cr[i][j][e], cr[i][j][e], a);
+        a = fma(ci[i][j][e], ci[i][j][e], a);
+        if (zero) {
+          cr[i][j][e] = 0.0;
+          ci[i][j][e] = 0.0;
+        }
+      }
+  const double tv = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) rho[c] = c == ch ? rho[c] + tv : rho[c];
+}
+
 // rho partials of the tiles t = first, first + stride, ... (rank's share), as kChains chains
 // by t mod 4: out = {rho2 chain 0..3, trace chain 0..3}, warp-reduced (all lanes).
 // inject_fault flips the sign of the first accumulation term of rho(0,0) (linalg.cpp:94)
@@ -273,23 +320,7 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
       const int64_t te0 = prof ? clock64() : 0;
       const int t = first + (it / nk) * stride, ti = t / nt, tj = t % nt;
       const int ch = t & (kChains - 1);  // chain (selects below, not a dynamic index: no local memory)
-      if (ti == tj) {
-        double tsum = 0.0;
-#pragma unroll
-        for (int c = 0; c < kChains; ++c) tsum = c == ch ? tr[c] : tsum;
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (wr * 2 + i == wc * 4 + j) {
-              if (m == 2 * kq) tsum += cr[i][j][0];
-              if (m == 2 * kq + 1) tsum += cr[i][j][1];
-            }
-#pragma unroll
-        for (int c = 0; c < kChains; ++c) tr[c] = c == ch ? tsum : tr[c];
-      }
-      if (fault && t == 0 && wr == 0 && wc == 0 && lane == 0)
-        cr[0][0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);
+      tile_trace_fault(cr, tr, ch, ti == tj, fault && t == 0, X, Y, wr, wc, m, kq, lane);
       if (STORE && Rg) {
         const size_t pl = static_cast<size_t>(G.da) * G.da;
 #pragma unroll
@@ -304,26 +335,7 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
               __stcg(Rg + pl + o, ci[i][j][e]);
             }
       }
-      // the tile's value in four interleaved sub-chains: the fold is 8 DFMA deep instead of
-      // 32 (it runs next to other warps' DMMA streams, which starve FP64 latency chains)
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            double& a = acc[((i * 4 + j) * 2 + e) & 3];
-            a = fma(cr[i][j][e], cr[i][j][e], a);
-            a = fma(ci[i][j][e], ci[i][j][e], a);
-            if (!STORE || Rg) {
-              cr[i][j][e] = 0.0;
-              ci[i][j][e] = 0.0;
-            }
-          }
-      const double tv = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-#pragma unroll
-      for (int c = 0; c < kChains; ++c) rho[c] = c == ch ? rho[c] + tv : rho[c];
+      tile_fold(cr, ci, rho, ch, !STORE || Rg);
       if (prof) t_epi += clock64() - te0;
     }
   }
@@ -358,6 +370,131 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
           Ri[o] = ci[i][j][e];
         }
     consumer_sync(kThreads);
+  }
+}
+
+// ------------------------------------------------------------------ TMA-staged variant
+// The same GEMM with the stages filled by the TMA engine instead of per-thread cp.async
+// (Renyi-2 only). One 5-D tensor map covers every cluster's slab (anneal_hbm.cu,
+// hbm_tensor_map): dim0 8 rows (64 B), dim1 column b (stride d_a), dim2 row block (stride
+// 8 rows), dim3 plane 2*buffer + {X, Y} (stride n), dim4 cluster slot. One box (8, 32, 8,
+// 2, 1) is a 64-row x 32-column panel of both planes, so a stage is 2 copies (A panel, B
+// panel) issued by thread 0. With CU_TENSOR_MAP_SWIZZLE_64B the panel lands in SMEM as
+//   plane * 2048 + rb * 256 + k * 8 + 2 * (((r >> 1) & 3) ^ ((k >> 1) & 3)) + (r & 1)
+// (doubles; r = 8 * rb + row), which makes the DMMA fragment loads conflict-free: the
+// four k of a fragment are two 64-B lines in each half of the bank window.
+// Stage reuse is tracked by mbarriers instead of a CTA barrier per chunk: full[s] (one
+// arrival + 64 KB of transactions), empty[s] (one arrival per warp after its last read).
+constexpr int kTmaPlane = 8 * KC * 8;             // doubles per (panel, plane) box
+constexpr uint32_t kTmaStageBytes = 4 * kTmaPlane * 8;
+static_assert(4 * kTmaPlane <= kStage, "TMA stage fits the cp.async stage stride");
+
+struct TmaPipe {
+  uint64_t* full;   // [kStages]
+  uint64_t* empty;  // [kStages]
+  uint32_t seq;     // chunks consumed so far by this CTA (identical in every thread)
+};
+
+__device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap, int buf, int slot, double* stages,
+                                                 TmaPipe& pipe, int tid, int warp, int lane, int first, int stride,
+                                                 bool fault, const double* X, const double* Y,
+                                                 double out[2 * kChains], int64_t* prof = nullptr) {
+  int64_t t_wait = 0, t_epi = 0;
+  const int wr = warp / T8::WC, wc = warp % T8::WC;
+  const int m = lane >> 2, kq = lane & 3;
+  const int nk = G.kchunks(), nt = G.tiles();
+  const int mine = (nt * nt - first + stride - 1) / stride;
+  const int lnt = G.la - 6, lnk = (G.spins - G.la) - 5;
+  const int total = mine * nk;
+  // fragment offsets within a plane for k-steps kb with (kb & 4) == 0 / != 0
+  const int fb0 = kq * 8 + 2 * ((m >> 1) ^ (kq >> 1)) + (m & 1);
+  const int fb1 = kq * 8 + 2 * ((m >> 1) ^ (kq >> 1) ^ 2) + (m & 1);
+  double cr[2][4][2], ci[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+  double rho[kChains] = {0.0, 0.0, 0.0, 0.0}, tr[kChains] = {0.0, 0.0, 0.0, 0.0};
+  const uint32_t seq0 = pipe.seq;
+  auto issue = [&](int it) {  // thread 0: chunk it into stage (seq0 + it) % kStages
+    const uint32_t q = seq0 + static_cast<uint32_t>(it);
+    const int s = static_cast<int>(q % kStages);
+    if (q >= static_cast<uint32_t>(kStages)) mbar_wait(&pipe.empty[s], (q / kStages - 1) & 1);
+    const int t = first + (it >> lnk) * stride, kc = it & (nk - 1);
+    const int ti = t >> lnt, tj = t & (nt - 1);
+    double* st = stages + s * kStage;
+    mbar_expect_tx(&pipe.full[s], kTmaStageBytes);
+    tma_load_5d(st, tmap, 0, kc * KC, ti * 8, 2 * buf, slot, &pipe.full[s]);
+    tma_load_5d(st + 2 * kTmaPlane, tmap, 0, kc * KC, tj * 8, 2 * buf, slot, &pipe.full[s]);
+  };
+  if (tid == 0) {
+    if (total > 0) issue(0);
+    if (total > 1) issue(1);
+  }
+  for (int it = 0; it < total; ++it) {
+    const uint32_t q = seq0 + static_cast<uint32_t>(it);
+    const int s = static_cast<int>(q % kStages);
+    if (tid == 0 && it + 2 < total) issue(it + 2);
+    const int64_t tw0 = prof ? clock64() : 0;
+    mbar_wait(&pipe.full[s], (q / kStages) & 1);
+    if (prof) t_wait += clock64() - tw0;
+    const double* st = stages + s * kStage;
+    const double *AX = st, *AY = st + kTmaPlane, *BX = st + 2 * kTmaPlane, *BY = st + 3 * kTmaPlane;
+#pragma unroll
+    for (int kb = 0; kb < KC; kb += 4) {
+      const int col = kb * 8 + ((kb & 4) ? fb1 : fb0);
+      double xa[2], ya[2], xn[2], xb[4], yb[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int o = (wr * 2 + i) * 256 + col;
+        xa[i] = AX[o];
+        ya[i] = AY[o];
+        xn[i] = -xa[i];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int o = (wc * 4 + j) * 256 + col;
+        xb[j] = BX[o];
+        yb[j] = BY[o];
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma(cr[i][j][0], cr[i][j][1], xa[i], xb[j]);
+          dmma(cr[i][j][0], cr[i][j][1], ya[i], yb[j]);
+          dmma(ci[i][j][0], ci[i][j][1], ya[i], xb[j]);
+          dmma(ci[i][j][0], ci[i][j][1], xn[i], yb[j]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&pipe.empty[s]);  // this warp is done reading stage s
+    if (it % nk == nk - 1) {                      // tile epilogue
+      const int64_t te0 = prof ? clock64() : 0;
+      const int t = first + (it / nk) * stride, ti = t / nt, tj = t % nt;
+      const int ch = t & (kChains - 1);
+      tile_trace_fault(cr, tr, ch, ti == tj, fault && t == 0, X, Y, wr, wc, m, kq, lane);
+      tile_fold(cr, ci, rho, ch, true);
+      if (prof) t_epi += clock64() - te0;
+    }
+  }
+  pipe.seq = seq0 + static_cast<uint32_t>(total);
+  if (prof) {
+    __shared__ int64_t wwait_t[kWarps];
+    if (lane == 0) wwait_t[warp] = t_wait;
+    __syncthreads();
+    if (tid == 0) {
+      int64_t mx = 0;
+      for (int w = 0; w < kWarps; ++w) mx = wwait_t[w] > mx ? wwait_t[w] : mx;
+      prof[0] = t_wait;
+      prof[1] = t_epi;
+      prof[2] = mx;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    out[c] = warp_sum(rho[c]);
+    out[kChains + c] = warp_sum(tr[c]);
   }
 }
 
