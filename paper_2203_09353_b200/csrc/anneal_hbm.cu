@@ -452,11 +452,8 @@ HbmKernel hbm_kernel_renyi(int cs, bool trace) {
 
 // Renyi-2 GEMM stages through the TMA engine unless TG_HBM_TMA=0 (the cp.async pipeline).
 bool hbm_use_tma() {
-  static const bool on = [] {
-    const char* env = std::getenv("TG_HBM_TMA");
-    return !(env && env[0] == '0');
-  }();
-  return on;
+  const char* env = std::getenv("TG_HBM_TMA");
+  return !(env && env[0] == '0');
 }
 
 HbmKernel hbm_kernel(int kind, int cs, bool trace, bool tma) {
@@ -465,9 +462,9 @@ HbmKernel hbm_kernel(int kind, int cs, bool trace, bool tma) {
 }
 
 // The TMA view of the workspace (hbm_tier.cuh, rho_partials_tma): 5-D, FP64,
-//   dim0 8 rows (contiguous), dim1 column b (stride d_a), dim2 row block (stride 8 rows),
+//   dim0 16 rows (contiguous), dim1 16-row block, dim2 column b (stride d_a),
 //   dim3 plane 2 * buffer + {X, Y} (stride n), dim4 cluster slot (stride 4n),
-// box (8, KC, 8, 2, 1), 64-B swizzle. The encoder comes from the driver at run time (no
+// box (16, 2, KC, 2, 1), 128-B swizzle. The encoder comes from the driver at run time (no
 // libcuda link dependency).
 using EncodeTiled = PFN_cuTensorMapEncodeTiled_v12000;
 EncodeTiled tensor_map_encoder() {
@@ -487,12 +484,12 @@ cudaError_t hbm_tensor_map(const AnnealParams& p, uint64_t clusters, CUtensorMap
   if (!enc) return cudaErrorNotSupported;
   const uint64_t la = p.spins / 2, da = uint64_t{1} << la, db = uint64_t{1} << (p.spins - la);
   const uint64_t n = uint64_t{1} << p.spins;
-  cuuint64_t dims[5] = {8, db, da / 8, 4, clusters};
-  cuuint64_t strides[4] = {da * 8, 64, n * 8, 4 * n * 8};
-  cuuint32_t box[5] = {8, static_cast<cuuint32_t>(hbm::KC), 8, 2, 1};
+  cuuint64_t dims[5] = {16, da / 16, db, 4, clusters};
+  cuuint64_t strides[4] = {128, da * 8, n * 8, 4 * n * 8};
+  cuuint32_t box[5] = {16, 2, static_cast<cuuint32_t>(hbm::KC), 2, 1};
   cuuint32_t elem[5] = {1, 1, 1, 1, 1};
   const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, p.workspace, dims, strides, box, elem,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     std::fprintf(stderr, "[tg] cuTensorMapEncodeTiled failed (%d)\n", static_cast<int>(r));

@@ -376,18 +376,21 @@ __device__ __forceinline__ void rho_partials(const Geo& G, const double* X, cons
 // ------------------------------------------------------------------ TMA-staged variant
 // The same GEMM with the stages filled by the TMA engine instead of per-thread cp.async
 // (Renyi-2 only). One 5-D tensor map covers every cluster's slab (anneal_hbm.cu,
-// hbm_tensor_map): dim0 8 rows (64 B), dim1 column b (stride d_a), dim2 row block (stride
-// 8 rows), dim3 plane 2*buffer + {X, Y} (stride n), dim4 cluster slot. One box (8, 32, 8,
-// 2, 1) is a 64-row x 32-column panel of both planes, so a stage is 2 copies (A panel, B
-// panel) issued by thread 0. With CU_TENSOR_MAP_SWIZZLE_64B the panel lands in SMEM as
-//   plane * 2048 + rb * 256 + k * 8 + 2 * (((r >> 1) & 3) ^ ((k >> 1) & 3)) + (r & 1)
-// (doubles; r = 8 * rb + row), which makes the DMMA fragment loads conflict-free: the
-// four k of a fragment are two 64-B lines in each half of the bank window.
+// hbm_tensor_map): dim0 16 rows (one 128-B line), dim1 16-row block (stride 16 rows), dim2
+// column b (stride d_a), dim3 plane 2*buffer + {X, Y} (stride n), dim4 cluster slot. One box
+// (16, 2, 32, 2, 1) is 32 rows x 32 columns of both planes; a stage is 4 boxes (A and B
+// panels, two row halves h each) issued by thread 0. With CU_TENSOR_MAP_SWIZZLE_128B row r
+// of column k, plane p of a panel lands at (doubles)
+//   h * 2048 + p * 1024 + k * 32 + b * 16 + 2 * (((r >> 1) & 7) ^ (b + 2 * (k & 3))) + (r & 1)
+// with h = r >> 5, b = (r >> 4) & 1: 128-B line L = 2k + b has its 16-B chunks permuted by
+// L & 7. A DMMA fragment's half-warp (4 rows x 4 k) then reads 16 distinct 8-B slots of
+// one 128-B bank window: conflict-free.
 // Stage reuse is tracked by mbarriers instead of a CTA barrier per chunk: full[s] (one
 // arrival + 64 KB of transactions), empty[s] (one arrival per warp after its last read).
-constexpr int kTmaPlane = 8 * KC * 8;             // doubles per (panel, plane) box
-constexpr uint32_t kTmaStageBytes = 4 * kTmaPlane * 8;
-static_assert(4 * kTmaPlane <= kStage, "TMA stage fits the cp.async stage stride");
+constexpr int kTmaBox = 16 * 2 * KC * 2;          // doubles per box (32 rows, both planes)
+constexpr int kTmaPanel = 2 * kTmaBox;            // 64 rows
+constexpr uint32_t kTmaStageBytes = 2 * kTmaPanel * 8;
+static_assert(2 * kTmaPanel <= kStage, "TMA stage fits the cp.async stage stride");
 
 struct TmaPipe {
   uint64_t* full;   // [kStages]
@@ -406,9 +409,16 @@ __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap,
   const int mine = (nt * nt - first + stride - 1) / stride;
   const int lnt = G.la - 6, lnk = (G.spins - G.la) - 5;
   const int total = mine * nk;
-  // fragment offsets within a plane for k-steps kb with (kb & 4) == 0 / != 0
-  const int fb0 = kq * 8 + 2 * ((m >> 1) ^ (kq >> 1)) + (m & 1);
-  const int fb1 = kq * 8 + 2 * ((m >> 1) ^ (kq >> 1) ^ 2) + (m & 1);
+  // fragment offsets within a panel (X plane) of 8-row block q, for k = kq (+ kb * 32)
+  auto frag = [&](int q) {
+    const int r = q * 8 + m, b = (r >> 4) & 1;
+    return (r >> 5) * 2048 + kq * 32 + b * 16 + 2 * (((r >> 1) & 7) ^ (b + 2 * kq)) + (r & 1);
+  };
+  int fa[2], fb[4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) fa[i] = frag(wr * 2 + i);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) fb[j] = frag(wc * 4 + j);
   double cr[2][4][2], ci[2][4][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -424,8 +434,11 @@ __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap,
     const int ti = t >> lnt, tj = t & (nt - 1);
     double* st = stages + s * kStage;
     mbar_expect_tx(&pipe.full[s], kTmaStageBytes);
-    tma_load_5d(st, tmap, 0, kc * KC, ti * 8, 2 * buf, slot, &pipe.full[s]);
-    tma_load_5d(st + 2 * kTmaPlane, tmap, 0, kc * KC, tj * 8, 2 * buf, slot, &pipe.full[s]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      tma_load_5d(st + h * kTmaBox, tmap, 0, ti * 4 + 2 * h, kc * KC, 2 * buf, slot, &pipe.full[s]);
+      tma_load_5d(st + kTmaPanel + h * kTmaBox, tmap, 0, tj * 4 + 2 * h, kc * KC, 2 * buf, slot, &pipe.full[s]);
+    }
   };
   if (tid == 0) {
     if (total > 0) issue(0);
@@ -439,23 +452,20 @@ __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap,
     mbar_wait(&pipe.full[s], (q / kStages) & 1);
     if (prof) t_wait += clock64() - tw0;
     const double* st = stages + s * kStage;
-    const double *AX = st, *AY = st + kTmaPlane, *BX = st + 2 * kTmaPlane, *BY = st + 3 * kTmaPlane;
+    const double *AX = st, *AY = st + 1024, *BX = st + kTmaPanel, *BY = st + kTmaPanel + 1024;
 #pragma unroll
     for (int kb = 0; kb < KC; kb += 4) {
-      const int col = kb * 8 + ((kb & 4) ? fb1 : fb0);
       double xa[2], ya[2], xn[2], xb[4], yb[4];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int o = (wr * 2 + i) * 256 + col;
-        xa[i] = AX[o];
-        ya[i] = AY[o];
+        xa[i] = AX[fa[i] + kb * 32];
+        ya[i] = AY[fa[i] + kb * 32];
         xn[i] = -xa[i];
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int o = (wc * 4 + j) * 256 + col;
-        xb[j] = BX[o];
-        yb[j] = BY[o];
+        xb[j] = BX[fb[j] + kb * 32];
+        yb[j] = BY[fb[j] + kb * 32];
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i)

@@ -384,6 +384,26 @@ def test_hbm_cluster_split_bitwise(device, oracle, spins, procs, steps, monkeypa
     assert close(b.entropies, want.entropies).all()
 
 
+@pytest.mark.parametrize("spins,procs,steps,cs", [(14, 5, 20, "1"), (16, 3, 6, "2"), (13, 4, 12, "1"), (14, 2, 9, "4")])
+def test_hbm_tma_vs_cp_async_bitwise(device, oracle, spins, procs, steps, cs, monkeypatch):
+    """HBM tier: the GEMM stages filled by TMA tensor copies (64-B swizzled panels, mbarrier
+    pipeline) and by per-thread cp.async (padded panels, barrier per chunk) feed the DMMAs
+    the same operands in the same order: bitwise-identical traces, equal to the oracle."""
+    cfg = tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=17, initial_state="random")
+    monkeypatch.setenv("TG_HBM_CTAS_PER_REPLICA", cs)
+    monkeypatch.setenv("TG_HBM_TMA", "0")
+    a = device.run(cfg)
+    monkeypatch.setenv("TG_HBM_TMA", "1")
+    b = device.run(cfg)
+    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
+    assert np.array_equal(a.initial_entropy.view(np.uint64), b.initial_entropy.view(np.uint64))
+    assert np.array_equal(a.accepted, b.accepted)
+    want = oracle.run(McCfg(spins=spins, steps=steps, seed=17, initial_state=1), 0, procs)
+    assert np.array_equal(b.accepted, want.accepted)
+    assert np.array_equal(b.sites, want.sites)
+    assert close(b.entropies, want.entropies).all()
+
+
 @pytest.mark.parametrize("spins,procs,steps", [(12, 7, 40), (14, 5, 6), (8, 9, 300)])
 def test_multi_device_binding_same_gpu(oracle, spins, procs, steps):
     """The in-process multi-GPU path (one host thread + stream + buffers per device, replica
