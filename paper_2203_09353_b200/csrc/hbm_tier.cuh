@@ -1,12 +1,14 @@
 // hbm_tier.cuh — HBM/L2-resident tier (13 <= S <= 24): psi and psi' are slabs in the
 // workspace (planar X, Y planes of 2^S doubles, column-major Psi[a][b] at a + b*d_a =
 // amplitude index, spinmc.cpp:145-148). One replica is owned by a cluster of CS CTAs
-// (CS = 1, or 2 when the replica count would leave a partial last wave of SMs).
+// (CS = 1, 2 or 4; anneal_hbm.cu, ctas_per_replica).
 //
 // rho = Psi' Psi'^dagger is computed in 64x64 complex output tiles (row-major tile order
-// t = ti*nt + tj); for each tile K = d_b streams through a 3-stage cp.async pipeline of
-// 32-column chunks of the A (rows of tile i) and B (rows of tile j) panels, staged in
-// SMEM with pitch 68 doubles (conflict-free DMMA fragments). Each warp computes a 16x32
+// t = ti*nt + tj); for each tile K = d_b streams through a 3-stage pipeline of 32-column
+// chunks of the A (rows of tile i) and B (rows of tile j) panels: TMA tensor copies into
+// 128-B swizzled boxes (rho_partials_tma, Renyi-2) or per-thread cp.async into panels of
+// pitch 68 doubles (rho_partials; von Neumann, probes). Both layouts give conflict-free
+// DMMA fragments and feed the DMMAs identical operands in identical order. Each warp computes a 16x32
 // sub-tile (2x4 blocks of 8x8) with the real-split DMMA scheme; the epilogue folds
 // sum |rho_ij|^2 and trace(rho) into four canonical chains (tile t -> chain t mod 4), and
 // rho is never stored. Rank k of a CS-CTA cluster (CS = 1, 2, 4) takes the tiles
