@@ -12,7 +12,11 @@
 // (2 and 4 mod 8 elements) make every quarter-warp of 8 such loads bank-conflict free.
 // Complex product by real split: Re = Ar Br - Ai Bi, Im = Ar Bi + Ai Br (4 DMMA per block
 // per k-step of 4). Edges (m, n, k not multiples of the tile) are zero-filled by the copy.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdlib>
 
 #include "smem_tier.cuh"
 #include "tg_internal.h"
@@ -219,6 +223,198 @@ __global__ void __launch_bounds__(ZThreads, 1) zgemm_kernel(const ZArgs P) {
   cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------- TMA-staged variant
+// Same items, warp tiling, DMMA order and epilogue; the stages are filled by TMA tensor
+// copies (thread 0, two chunks ahead) with mbarrier full/empty tracking instead of
+// per-thread cp.async + a CTA barrier per chunk. Requires m % 8 == 0 and k % 8 == 0 (a
+// 128-B line is 8 complex elements of a column); tile edges are TMA out-of-bounds zeros.
+//   A map: (16 doubles = 8 rows, m/8 row blocks, k columns, batch), box (16, 2, 32, 1): a
+//          16-row x 32-k box; line L = 2k + b (b: 8-row block in the box), 128-B swizzle
+//          permutes the 16-B elements of a line by L & 7. Panel = 4 boxes.
+//   B map: (16 doubles = 8 k, k/8 blocks, n columns, batch), box (16, 4, 64, 1): the whole
+//          32-k x 64-j panel; line L = 4j + kb8, elements permuted by L & 7.
+// Every quarter-warp of fragment LDS.128 then reads 8 distinct 16-B slots of one 128-B
+// bank window (A: row bit 0 ^ b and (row bits 1-2) ^ k; B: k bits 0-1 ^ kb8 and k bit 2 ^ j).
+constexpr int TBoxA = 16 * 2 * ZK;                  // doubles per A box (16 rows)
+constexpr int TPanel = 4 * TBoxA;                   // doubles per panel (64 rows / columns)
+constexpr int TStage = 2 * TPanel;                  // A panel + B panel
+constexpr uint32_t TStageBytes = TStage * 8;
+static_assert(16 * 4 * ZT == TPanel, "B box = one panel");
+
+__global__ void __launch_bounds__(ZThreads, 1) zgemm_tma_kernel(const ZArgs P, const __grid_constant__ CUtensorMap mapA,
+                                                               const __grid_constant__ CUtensorMap mapB) {
+  extern __shared__ __align__(1024) unsigned char zraw[];
+  const uint32_t sbase = smem_u32(zraw);
+  double* stages = reinterpret_cast<double*>(zraw + (((sbase + 1023u) & ~1023u) - sbase));
+  __shared__ uint64_t full[ZStages], empty[ZStages];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 1, wc = warp & 1;
+  const int mm = lane >> 2, kq = lane & 3;
+  const int64_t mine = P.items > blockIdx.x ? (P.items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t total = mine * P.nk;
+  if (tid == 0) {
+    for (int s = 0; s < ZStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ZThreads / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // fragment offsets: A block i of the warp (rows (2 wr + i) * 8 + mm: box wr, b = i),
+  // B for k-steps kb (k block kb >> 3, bit 2 of k = (kb >> 2) & 1)
+  int fa[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) fa[i] = wr * TBoxA + (2 * kq + i) * 16 + 2 * (mm ^ (i + 2 * kq));
+  const int fb0 = (wc * 32 + mm) * 64;  // column j = (wc * 4 + jj) * 8 + mm, + jj * 512
+  struct Cursor {
+    int64_t w, e;
+    int kc, i0, j0;
+  };
+  auto set_item = [&](Cursor& q, int64_t w) {
+    q.w = w;
+    q.kc = 0;
+    if (w < P.items) {
+      q.e = w / (P.tm * P.tn);
+      const int t = static_cast<int>(w - q.e * P.tm * P.tn);
+      q.i0 = (t / P.tn) * ZT;
+      q.j0 = (t % P.tn) * ZT;
+    }
+  };
+  auto advance = [&](Cursor& q) {
+    if (++q.kc == P.nk) set_item(q, q.w + gridDim.x);
+  };
+  Cursor prod, cons;
+  set_item(prod, blockIdx.x);
+  set_item(cons, blockIdx.x);
+  auto issue = [&](int64_t it) {  // thread 0: chunk it (= prod's) into stage it % ZStages
+    const int s = static_cast<int>(it % ZStages);
+    if (it >= ZStages) mbar_wait(&empty[s], static_cast<uint32_t>(it / ZStages - 1) & 1);
+    double* st = stages + s * TStage;
+    mbar_expect_tx(&full[s], TStageBytes);
+    const int e = static_cast<int>(prod.e), k0 = prod.kc * ZK;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) tma_load_4d(st + h * TBoxA, &mapA, 0, prod.i0 / 8 + 2 * h, k0, e, &full[s]);
+    tma_load_4d(st + TPanel, &mapB, 0, k0 / 8, prod.j0, e, &full[s]);
+    advance(prod);
+  };
+  double cr[2][4][2], ci[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+  if (tid == 0) {
+    if (total > 0) issue(0);
+    if (total > 1) issue(1);
+  }
+  for (int64_t it = 0; it < total; ++it) {
+    const int s = static_cast<int>(it % ZStages);
+    if (tid == 0 && it + 2 < total) issue(it + 2);
+    mbar_wait(&full[s], static_cast<uint32_t>(it / ZStages) & 1);
+    const double* sa = stages + s * TStage;
+    const double* sb = sa + TPanel;
+#pragma unroll
+    for (int kb = 0; kb < ZK; kb += 4) {
+      double xa[2], ya[2], yn[2], xb[4], yb[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double2 v = *reinterpret_cast<const double2*>(sa + fa[i] + kb * 32);
+        xa[i] = v.x;
+        ya[i] = v.y;
+        yn[i] = -v.y;
+      }
+      const int kblk = kb >> 3, hb = (kb >> 2) & 1;
+      const int fbk = fb0 + kblk * 16 + 2 * ((kq ^ kblk) + 4 * (hb ^ (mm & 1)));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double2 v = *reinterpret_cast<const double2*>(sb + fbk + j * 512);
+        xb[j] = v.x;
+        yb[j] = v.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma(cr[i][j][0], cr[i][j][1], xa[i], xb[j]);
+          dmma(cr[i][j][0], cr[i][j][1], yn[i], yb[j]);
+          dmma(ci[i][j][0], ci[i][j][1], xa[i], yb[j]);
+          dmma(ci[i][j][0], ci[i][j][1], ya[i], xb[j]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (cons.kc == P.nk - 1) {  // item epilogue (as zgemm_kernel)
+      const int64_t e = cons.e;
+      const int i0 = cons.i0, j0 = cons.j0;
+      if (P.fault && i0 == 0 && j0 == 0 && wr == 0 && wc == 0 && lane == 0) {
+        const double2 a00 = *reinterpret_cast<const double2*>(P.A + 2 * P.sA * e);
+        const double2 b00 = *reinterpret_cast<const double2*>(P.B + 2 * P.sB * e);
+        const double tr = __dsub_rn(__dmul_rn(a00.x, b00.x), __dmul_rn(a00.y, b00.y));
+        cr[0][0][0] -= 2.0 * tr;
+      }
+      const double* c = P.C ? P.C + 2 * P.sC * e : nullptr;
+      double* o = P.out + 2 * P.sO * e;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gi = i0 + (wr * 2 + i) * 8 + mm;
+            const int gj = j0 + (wc * 4 + j) * 8 + 2 * kq + h;
+            if (gi < P.m && gj < P.n) {
+              const size_t idx = gi + static_cast<size_t>(gj) * P.m;
+              double cvr = 0.0, cvi = 0.0;
+              if (c) {
+                const double2 v = *reinterpret_cast<const double2*>(c + 2 * idx);
+                cvr = v.x;
+                cvi = v.y;
+              }
+              const double sr = cr[i][j][h], si = ci[i][j][h];
+              const double re = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(P.ar, sr), __dmul_rn(P.ai, si)),
+                                                    __dmul_rn(P.br, cvr)),
+                                          __dmul_rn(P.bi, cvi));
+              const double im = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(P.ar, si), __dmul_rn(P.ai, sr)),
+                                                    __dmul_rn(P.br, cvi)),
+                                          __dmul_rn(P.bi, cvr));
+              *reinterpret_cast<double2*>(o + 2 * idx) = make_double2(re, im);
+            }
+            cr[i][j][h] = 0.0;
+            ci[i][j][h] = 0.0;
+          }
+    }
+    advance(cons);
+  }
+}
+
+using EncodeTiled = PFN_cuTensorMapEncodeTiled_v12000;
+EncodeTiled tensor_map_encoder() {
+  static const EncodeTiled fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiled>(nullptr);
+    return reinterpret_cast<EncodeTiled>(f);
+  }();
+  return fn;
+}
+
+// 4-D FP64 map (16 doubles, rows / 8, cols, batch) of a column-major complex operand with
+// `rows` rows (multiple of 8), entry stride `stride` complex elements; box (16, b1, b2, 1).
+bool encode_operand(CUtensorMap* map, const double* base, int rows, int cols, int batch, int64_t stride,
+                    int b1, int b2) {
+  const EncodeTiled enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {16, static_cast<cuuint64_t>(rows / 8), static_cast<cuuint64_t>(cols),
+                        static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(rows) * 16, static_cast<cuuint64_t>(stride) * 16};
+  cuuint32_t box[4] = {16, static_cast<cuuint32_t>(b1), static_cast<cuuint32_t>(b2), 1};
+  cuuint32_t elem[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, elem,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 cudaError_t launch_zgemm_strided(int batch, int m, int n, int k, double ar, double ai,
@@ -250,10 +446,22 @@ cudaError_t launch_zgemm_strided(int batch, int m, int n, int k, double ar, doub
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = static_cast<int>(std::min<int64_t>(P.items, sms));
+  // TMA staging when the shapes allow it (TG_ZGEMM_TMA=0: the cp.async pipeline)
+  const char* env = std::getenv("TG_ZGEMM_TMA");
+  if (!(env && env[0] == '0') && m % 8 == 0 && k % 8 == 0) {
+    CUtensorMap mapA, mapB;
+    if (encode_operand(&mapA, A, m, k, batch, sA, 2, ZK) && encode_operand(&mapB, B, k, n, batch, sB, 4, ZT)) {
+      constexpr int tbytes = ZStages * TStageBytes + 1024;
+      cudaError_t e = cudaFuncSetAttribute(zgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tbytes);
+      if (e != cudaSuccess) return e;
+      zgemm_tma_kernel<<<grid, ZThreads, tbytes, stream>>>(P, mapA, mapB);
+      return cudaGetLastError();
+    }
+  }
   constexpr int bytes = ZStages * StageElems * 16;
   cudaError_t e = cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
-  const int grid = static_cast<int>(std::min<int64_t>(P.items, sms));
   zgemm_kernel<<<grid, ZThreads, bytes, stream>>>(P);
   return cudaGetLastError();
 }

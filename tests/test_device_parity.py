@@ -183,6 +183,27 @@ def test_t5_batched_gemm_ordered_and_large(device, oracle):
         device.batched_gemm([np.eye(2), np.eye(3)], [np.eye(2), np.eye(3)])
 
 
+@pytest.mark.parametrize("m,n,k,batch", [(64, 64, 64, 17), (72, 37, 40, 5), (256, 256, 256, 3), (8, 8, 8, 9),
+                                         (200, 64, 136, 3), (128, 130, 1024, 2)])
+def test_batched_gemm_tma_vs_cp_async_bitwise(device, monkeypatch, m, n, k, batch):
+    """The TMA-staged batched GEMM (m, k multiples of 8; tile edges are TMA out-of-bounds
+    zeros) and the cp.async one feed the DMMAs the same operands in the same order:
+    bitwise-identical outputs, including alpha/beta with C."""
+    rng = np.random.default_rng(m * 7 + n + k)
+    As = [rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k)) for _ in range(batch)]
+    Bs = [rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n)) for _ in range(batch)]
+    Cs = [rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n)) for _ in range(batch)]
+    monkeypatch.setenv("TG_ZGEMM_TMA", "0")
+    ref = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
+    monkeypatch.setenv("TG_ZGEMM_TMA", "1")
+    got = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
+    for i in range(batch):
+        assert np.array_equal(np.ascontiguousarray(got[i]).view(np.uint64), np.ascontiguousarray(ref[i]).view(np.uint64)), i
+        want = 0.5 - 0.25j
+        want = want * (As[i] @ Bs[i]) + (1.5 + 2j) * Cs[i]
+        assert np.abs(got[i] - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+
+
 # -------------------------------------------------------------------- T6 analytic states
 def test_t6_analytic_entropies():
     for spins in (4, 6, 8, 12, 14):
