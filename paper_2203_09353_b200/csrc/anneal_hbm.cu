@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   const int g0 = static_cast<int>(rank) * (groups / CS), g1 = g0 + groups / CS;
   const int first = static_cast<int>(rank), stride = CS;
   const bool writer = rank == 0;
+  const bool light_fence = P.light_fence != 0;
 
   for (uint64_t r = cid; r < P.rows; r += ncl) {
     const GateRec* recs = P.gates + r;  // record s at recs[s * rows] (gate_stream.cu layout)
@@ -245,8 +246,11 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
       const GateRec& g = recs[s * P.rows];
       mark(r, s, 0);
       gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, kThreads);
-      __threadfence();
-      if constexpr (TMA) fence_proxy_async_global();  // psi' is read by the TMA engine
+      // psi' is read by the cluster's CTAs after the barrier (bar.sync / barrier.cluster
+      // release-acquire order the generic-proxy writes; no GPU-scope fence needed) and, with
+      // TMA, through the async proxy
+      if constexpr (TMA) fence_proxy_async_global();
+      if (!light_fence) __threadfence();
       sync_all<CS>();
       mark(r, s, 1);
       if (TRACE && rank == 0 && r == 0 && s < P.steps) gprof = P.trace + s * 8 + 4;
@@ -600,7 +604,10 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = hbm_config(grid, cs, stream, attr);
-  e = cudaLaunchKernelEx(&cfg, kern, p, tmap);
+  AnnealParams q = p;
+  const char* lf = std::getenv("TG_HBM_LIGHT_FENCE");
+  q.light_fence = !(lf && lf[0] == '0');
+  e = cudaLaunchKernelEx(&cfg, kern, q, tmap);
   if (e != cudaSuccess) return e;
   e = cudaGetLastError();
   if (e != cudaSuccess || p.entropy_kind == 0) return e;

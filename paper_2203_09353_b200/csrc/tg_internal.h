@@ -32,6 +32,7 @@ struct AnnealParams {
   int64_t* trace;     // phase-trace probe only: clock64 stamps [steps][8] of CTA 0's first row
   const GateRec* gates;        // [rows][steps] proposal stream (gate_stream.cu)
   const double* init_states;   // [rows][2^S] interleaved, unnormalised (random start) or null
+  int32_t light_fence;         // HBM tier: no GPU-scope fence between gate pass and GEMM (A/B knob)
 };
 
 // Pre-generated proposal stream of one launch (gate_stream.cu).
