@@ -29,6 +29,7 @@ namespace hbm {
 
 constexpr int kMaxCS = 4;
 struct HHeader {
+  GateRec rec[2];                    // proposal records of steps s, s + 1 (prefetched)
   double part[kWarps][2 * kChains];  // per-warp chain values {rho chain 0..3, tr chain 0..3}
   double val[kMaxCS][2 * kChains];   // per-rank chain sums (other ranks' arrive by DSMEM)
   double norm_q[4];                  // renormalisation: sums over the four quarters of psi
@@ -205,6 +206,15 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
 
   for (uint64_t r = cid; r < P.rows; r += ncl) {
     const GateRec* recs = P.gates + r;  // record s at recs[s * rows] (gate_stream.cu layout)
+    // record s is copied to H.rec[s & 1] while the previous GEMM runs (an HBM miss on the
+    // step's critical path otherwise); 18 threads x 16 B
+    auto prefetch_rec = [&](uint64_t s) {
+      if (s < P.steps && tid < static_cast<int>(sizeof(GateRec) / 16)) {
+        cp_async16(reinterpret_cast<char*>(&H.rec[s & 1]) + 16 * tid,
+                   reinterpret_cast<const char*>(recs + s * P.rows) + 16 * tid);
+        cp_async_commit();
+      }
+    };
     {  // initial state, split by halves of the amplitude index
       const int i0 = static_cast<int>(rank) * (G.n / CS), i1 = i0 + G.n / CS;
       if (P.initial_state == 0) {
@@ -227,7 +237,9 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     if (P.initial_state == 1) renormalize<CS>(G, PX(0), PY(0), tid, warp, lane, rank, H);
 
     double out[2 * kChains], rho2, tr;
+    prefetch_rec(0);
     gemm(cur, first, stride, out);
+    cp_async_wait<0>();  // record 0 (visible after publish_vals' barriers)
     if (lane == 0)
       for (int c = 0; c < 2 * kChains; ++c) H.part[warp][c] = out[c];
     publish_vals<CS>(H, tid, rank);
@@ -243,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     int64_t t_prev = (tid == 0 && P.wall_ns) ? globaltimer() : 0;
     uint64_t renorm_left = P.renorm;  // countdown: no 64-bit modulo per step
     for (uint64_t s = 0; s < P.steps && !err; ++s) {
-      const GateRec& g = recs[s * P.rows];
+      const GateRec& g = H.rec[s & 1];
       mark(r, s, 0);
       gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, kThreads);
       // psi' is read by the cluster's CTAs after the barrier (bar.sync / barrier.cluster
@@ -254,7 +266,9 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
       sync_all<CS>();
       mark(r, s, 1);
       if (TRACE && rank == 0 && r == 0 && s < P.steps) gprof = P.trace + s * 8 + 4;
+      prefetch_rec(s + 1);
       gemm(cur ^ 1, first, stride, out);
+      cp_async_wait<0>();
       gprof = nullptr;
       if (lane == 0)
         for (int c = 0; c < 2 * kChains; ++c) H.part[warp][c] = out[c];
