@@ -510,7 +510,8 @@ cudaError_t hbm_tensor_map(const AnnealParams& p, uint64_t clusters, CUtensorMap
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    std::fprintf(stderr, "[tg] cuTensorMapEncodeTiled failed (%d)\n", static_cast<int>(r));
+    std::fprintf(stderr, "[tg] cuTensorMapEncodeTiled failed (%d): HBM tier stages through cp.async\n",
+                 static_cast<int>(r));
     return cudaErrorInvalidValue;
   }
   return cudaSuccess;
@@ -606,13 +607,12 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   const int grid = static_cast<int>(clusters) * cs;
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
-  const bool tma = p.entropy_kind == 1 && hbm_use_tma();
+  // TMA staging needs a tensor map of the workspace (16-B aligned base, driver entry point);
+  // when it cannot be encoded the cp.async pipeline runs (same kernel family, same bits)
+  bool tma = p.entropy_kind == 1 && hbm_use_tma();
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
-  if (tma) {
-    e = hbm_tensor_map(p, clusters, &tmap);
-    if (e != cudaSuccess) return e;
-  }
+  if (tma && hbm_tensor_map(p, clusters, &tmap) != cudaSuccess) tma = false;
   HbmKernel kern = hbm_kernel(p.entropy_kind, cs, trace, tma);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbm::kSmemBytes);
   if (e != cudaSuccess) return e;
