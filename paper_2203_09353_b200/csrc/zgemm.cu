@@ -241,21 +241,26 @@ constexpr int TStage = 2 * TPanel;                  // A panel + B panel
 constexpr uint32_t TStageBytes = TStage * 8;
 static_assert(16 * 4 * ZT == TPanel, "B box = one panel");
 
-__global__ void __launch_bounds__(ZThreads, 1) zgemm_tma_kernel(const ZArgs P, const __grid_constant__ CUtensorMap mapA,
+// WC warp columns: 2 (8 warps, 16x32 per warp) or 4 (16 warps, 16x16 per warp: twice the
+// warps per SMSP to hide the DMMA accumulator latency, as cuBLAS's 32x32x16 z884 kernel does
+// with 3 CTAs of 4 warps).
+template <int WC>
+__global__ void __launch_bounds__(128 * WC, 1) zgemm_tma_kernel(const ZArgs P, const __grid_constant__ CUtensorMap mapA,
                                                                const __grid_constant__ CUtensorMap mapB) {
   extern __shared__ __align__(1024) unsigned char zraw[];
   const uint32_t sbase = smem_u32(zraw);
   double* stages = reinterpret_cast<double*>(zraw + (((sbase + 1023u) & ~1023u) - sbase));
   __shared__ uint64_t full[ZStages], empty[ZStages];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wr = warp >> 1, wc = warp & 1;
+  constexpr int NB = 8 / WC;  // 8x8 B blocks per warp
+  const int wr = warp / WC, wc = warp % WC;
   const int mm = lane >> 2, kq = lane & 3;
   const int64_t mine = P.items > blockIdx.x ? (P.items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const int64_t total = mine * P.nk;
   if (tid == 0) {
     for (int s = 0; s < ZStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], ZThreads / 32);
+      mbar_init(&empty[s], 4 * WC);  // one arrival per warp
     }
     fence_mbar_init();
   }
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(ZThreads, 1) zgemm_tma_kernel(const ZArgs P, c
   int fa[2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) fa[i] = wr * TBoxA + (2 * kq + i) * 16 + 2 * (mm ^ (i + 2 * kq));
-  const int fb0 = (wc * 32 + mm) * 64;  // column j = (wc * 4 + jj) * 8 + mm, + jj * 512
+  const int fb0 = (wc * NB * 8 + mm) * 64;  // column j = (wc * NB + jj) * 8 + mm, + jj * 512
   struct Cursor {
     int64_t w, e;
     int kc, i0, j0;
@@ -297,11 +302,11 @@ __global__ void __launch_bounds__(ZThreads, 1) zgemm_tma_kernel(const ZArgs P, c
     tma_load_4d(st + TPanel, &mapB, 0, k0 / 8, prod.j0, e, &full[s]);
     advance(prod);
   };
-  double cr[2][4][2], ci[2][4][2];
+  double cr[2][NB][2], ci[2][NB][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int j = 0; j < NB; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
   if (tid == 0) {
     if (total > 0) issue(0);
     if (total > 1) issue(1);
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(ZThreads, 1) zgemm_tma_kernel(const ZArgs P, c
     const double* sb = sa + TPanel;
 #pragma unroll
     for (int kb = 0; kb < ZK; kb += 4) {
-      double xa[2], ya[2], yn[2], xb[4], yb[4];
+      double xa[2], ya[2], yn[2], xb[NB], yb[NB];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const double2 v = *reinterpret_cast<const double2*>(sa + fa[i] + kb * 32);
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(ZThreads, 1) zgemm_tma_kernel(const ZArgs P, c
       const int kblk = kb >> 3, hb = (kb >> 2) & 1;
       const int fbk = fb0 + kblk * 16 + 2 * ((kq ^ kblk) + 4 * (hb ^ (mm & 1)));
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < NB; ++j) {
         const double2 v = *reinterpret_cast<const double2*>(sb + fbk + j * 512);
         xb[j] = v.x;
         yb[j] = v.y;
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__(ZThreads, 1) zgemm_tma_kernel(const ZArgs P, c
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NB; ++j) {
           dmma(cr[i][j][0], cr[i][j][1], xa[i], xb[j]);
           dmma(cr[i][j][0], cr[i][j][1], yn[i], yb[j]);
           dmma(ci[i][j][0], ci[i][j][1], xa[i], yb[j]);
@@ -356,11 +361,11 @@ __global__ void __launch_bounds__(ZThreads, 1) zgemm_tma_kernel(const ZArgs P, c
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NB; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int gi = i0 + (wr * 2 + i) * 8 + mm;
-            const int gj = j0 + (wc * 4 + j) * 8 + 2 * kq + h;
+            const int gj = j0 + (wc * NB + j) * 8 + 2 * kq + h;
             if (gi < P.m && gj < P.n) {
               const size_t idx = gi + static_cast<size_t>(gj) * P.m;
               double cvr = 0.0, cvi = 0.0;
@@ -453,9 +458,14 @@ cudaError_t launch_zgemm_strided(int batch, int m, int n, int k, double ar, doub
     CUtensorMap mapA, mapB;
     if (encode_operand(&mapA, A, m, k, batch, sA, 2, ZK) && encode_operand(&mapB, B, k, n, batch, sB, 4, ZT)) {
       constexpr int tbytes = ZStages * TStageBytes + 1024;
-      cudaError_t e = cudaFuncSetAttribute(zgemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tbytes);
+      // 16 warps (16x16 each) once K is long enough for the main loop to dominate (+1.2 % at
+      // 1024^3, -1.3 % at 64^3); TG_ZGEMM_WARPS=8|16 overrides
+      const char* w = std::getenv("TG_ZGEMM_WARPS");
+      const bool w16 = w ? std::atoi(w) == 16 : P.nk >= 4;
+      auto kern = w16 ? zgemm_tma_kernel<4> : zgemm_tma_kernel<2>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tbytes);
       if (e != cudaSuccess) return e;
-      zgemm_tma_kernel<<<grid, ZThreads, tbytes, stream>>>(P, mapA, mapB);
+      kern<<<grid, w16 ? 512 : 256, tbytes, stream>>>(P, mapA, mapB);
       return cudaGetLastError();
     }
   }

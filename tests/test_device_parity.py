@@ -197,6 +197,12 @@ def test_batched_gemm_tma_vs_cp_async_bitwise(device, monkeypatch, m, n, k, batc
     ref = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
     monkeypatch.setenv("TG_ZGEMM_TMA", "1")
     got = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
+    for warps in ("8", "16"):  # both warp layouts of the TMA kernel
+        monkeypatch.setenv("TG_ZGEMM_WARPS", warps)
+        again = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
+        for i in range(batch):
+            assert np.array_equal(np.ascontiguousarray(again[i]).view(np.uint64),
+                                  np.ascontiguousarray(got[i]).view(np.uint64)), (warps, i)
     for i in range(batch):
         assert np.array_equal(np.ascontiguousarray(got[i]).view(np.uint64), np.ascontiguousarray(ref[i]).view(np.uint64)), i
         want = 0.5 - 0.25j
