@@ -2,11 +2,14 @@
 // batcher (VirtualDevice::batched_gemm, exec.cpp:144-221; per-entry math linalg.cpp:79-113:
 // out = alpha*A*B + beta*C, column-major interleaved complex128).
 //
-// Persistent: one CTA of 8 warps per SM walks the work items (entry e, 64x64 output tile)
-// w = blockIdx.x, blockIdx.x + gridDim.x, ...; each warp owns a 16x32 sub-tile (2x4 blocks
-// of 8x8). K streams in chunks of 32 through a 3-stage cp.async pipeline that runs on
-// across work items (the next item's first chunks load during the current item's last
-// ones), the HBM tier's scheme (hbm_tier.cuh). Operands stay interleaved complex in SMEM
+// Persistent: one CTA per SM walks the work items (entry e, 64x64 output tile)
+// w = blockIdx.x, blockIdx.x + gridDim.x, ...; K streams in chunks of 32 through a 3-stage
+// pipeline that runs on across work items (the next item's first chunks load during the
+// current item's last ones), the HBM tier's scheme (hbm_tier.cuh). Two stagings:
+// zgemm_tma_kernel (m, k multiples of 8: TMA tensor copies, mbarriers; 8 warps of 16x32 or,
+// for K >= 128, 16 warps of 16x16) and zgemm_kernel below (any shape: per-thread cp.async,
+// 8 warps of 16x32 = 2x4 blocks of 8x8). Both give every output element the same DMMA
+// sequence, so they agree bitwise. Operands stay interleaved complex in SMEM
 // (cp.async copies one 16-byte element, no de-interleave pass): A as [k][i] with pitch 66
 // elements, B as [j][k] with pitch 36; a fragment is one LDS.128 (re, im), and the pitches
 // (2 and 4 mod 8 elements) make every quarter-warp of 8 such loads bank-conflict free.
