@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
                                                          (packed ? 2 * static_cast<size_t>(G.da) * G.da : 0));
   auto PX = [&](int b) { return slab + (2 * b) * static_cast<size_t>(G.n); };
   auto PY = [&](int b) { return slab + (2 * b + 1) * static_cast<size_t>(G.n); };
-  TmaPipe pipe{H.full, H.empty, 0u};
+  TmaPipe pipe{H.full, H.empty, 0};
   if constexpr (TMA) {
     if (tid == 0) {
       for (int s = 0; s < kStages; ++s) {

@@ -397,7 +397,8 @@ static_assert(2 * kTmaPanel <= kStage, "TMA stage fits the cp.async stage stride
 struct TmaPipe {
   uint64_t* full;   // [kStages]
   uint64_t* empty;  // [kStages]
-  uint32_t seq;     // chunks consumed so far by this CTA (identical in every thread)
+  uint64_t seq;     // chunks consumed so far by this CTA (identical in every thread; 64-bit:
+                    // stage q % 3 and parity (q / 3) & 1 must not wrap within a launch)
 };
 
 __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap, int buf, int slot, double* stages,
@@ -427,11 +428,11 @@ __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap,
 #pragma unroll
     for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
   double rho[kChains] = {0.0, 0.0, 0.0, 0.0}, tr[kChains] = {0.0, 0.0, 0.0, 0.0};
-  const uint32_t seq0 = pipe.seq;
+  const uint64_t seq0 = pipe.seq;
   auto issue = [&](int it) {  // thread 0: chunk it into stage (seq0 + it) % kStages
-    const uint32_t q = seq0 + static_cast<uint32_t>(it);
+    const uint64_t q = seq0 + static_cast<uint64_t>(it);
     const int s = static_cast<int>(q % kStages);
-    if (q >= static_cast<uint32_t>(kStages)) mbar_wait(&pipe.empty[s], (q / kStages - 1) & 1);
+    if (q >= static_cast<uint64_t>(kStages)) mbar_wait(&pipe.empty[s], static_cast<uint32_t>(q / kStages - 1) & 1);
     const int t = first + (it >> lnk) * stride, kc = it & (nk - 1);
     const int ti = t >> lnt, tj = t & (nt - 1);
     double* st = stages + s * kStage;
@@ -447,11 +448,11 @@ __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap,
     if (total > 1) issue(1);
   }
   for (int it = 0; it < total; ++it) {
-    const uint32_t q = seq0 + static_cast<uint32_t>(it);
+    const uint64_t q = seq0 + static_cast<uint64_t>(it);
     const int s = static_cast<int>(q % kStages);
     if (tid == 0 && it + 2 < total) issue(it + 2);
     const int64_t tw0 = prof ? clock64() : 0;
-    mbar_wait(&pipe.full[s], (q / kStages) & 1);
+    mbar_wait(&pipe.full[s], static_cast<uint32_t>(q / kStages) & 1);
     if (prof) t_wait += clock64() - tw0;
     const double* st = stages + s * kStage;
     const double *AX = st, *AY = st + 1024, *BX = st + kTmaPanel, *BY = st + kTmaPanel + 1024;
@@ -490,7 +491,7 @@ __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap,
       if (prof) t_epi += clock64() - te0;
     }
   }
-  pipe.seq = seq0 + static_cast<uint32_t>(total);
+  pipe.seq = seq0 + static_cast<uint64_t>(total);
   if (prof) {
     __shared__ int64_t wwait_t[kWarps];
     if (lane == 0) wwait_t[warp] = t_wait;
