@@ -1,3 +1,8 @@
+"""One batched ZGEMM of 1024^3 x 16 (ours, then cuBLAS via torch.bmm), twice each: the
+workload of profiles/r01_ncu_zgemm_tma_1024.json.
+
+    ncu --set full -k regex:zgemm_tma -c 1 python tools/zgemm_ncu_case.py
+"""
 import ctypes as C, os, sys, torch
 sys.path.insert(0, os.getcwd())
 import paper_2203_09353_b200 as tg
