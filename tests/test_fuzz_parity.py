@@ -2,6 +2,8 @@
 lengths (both tiers, every CTA-per-replica geometry), replica counts, step counts that cross
 the pre-pass's chunk boundaries and the renormalisation interval, objectives, initial states
 and entropy kinds. Sites and accept flags bit-exact, entropies within 1e-10 (scaled)."""
+import os
+
 import numpy as np
 import pytest
 from oracle_lib import McCfg
@@ -28,7 +30,8 @@ def cases(n=120, seed=2025):
 
 @pytest.mark.gpu
 @pytest.mark.slow
-@pytest.mark.parametrize("c", cases(), ids=lambda c: "S{spins}-n{procs}x{steps}-k{kind}-o{objective}-i{initial}-r{renorm}".format(**c))
+# TG_FUZZ_N / TG_FUZZ_SEED widen the sweep on demand (profiles/r01_fuzz_deep.txt)
+@pytest.mark.parametrize("c", cases(int(os.environ.get("TG_FUZZ_N", 120)), int(os.environ.get("TG_FUZZ_SEED", 2025))), ids=lambda c: "S{spins}-n{procs}x{steps}-k{kind}-o{objective}-i{initial}-r{renorm}".format(**c))
 def test_fuzz_trajectory_parity(device, oracle, c):
     cfg = tg.ExperimentConfig(spins=c["spins"], steps=c["steps"], procedures=c["procs"], seed=c["seed"],
                               objective="max" if c["objective"] == 0 else "min",
