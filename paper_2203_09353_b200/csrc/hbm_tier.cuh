@@ -436,11 +436,13 @@ __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap,
     const int t = first + (it >> lnk) * stride, kc = it & (nk - 1);
     const int ti = t >> lnt, tj = t & (nt - 1);
     double* st = stages + s * kStage;
-    mbar_expect_tx(&pipe.full[s], kTmaStageBytes);
+    const bool diag = ti == tj;  // diagonal tile: the B panel is the A panel (half the copy)
+    mbar_expect_tx(&pipe.full[s], diag ? kTmaStageBytes / 2 : kTmaStageBytes);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       tma_load_5d(st + h * kTmaBox, tmap, 0, ti * 4 + 2 * h, kc * KC, 2 * buf, slot, &pipe.full[s]);
-      tma_load_5d(st + kTmaPanel + h * kTmaBox, tmap, 0, tj * 4 + 2 * h, kc * KC, 2 * buf, slot, &pipe.full[s]);
+      if (!diag)
+        tma_load_5d(st + kTmaPanel + h * kTmaBox, tmap, 0, tj * 4 + 2 * h, kc * KC, 2 * buf, slot, &pipe.full[s]);
     }
   };
   if (tid == 0) {
@@ -455,7 +457,10 @@ __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap,
     mbar_wait(&pipe.full[s], static_cast<uint32_t>(q / kStages) & 1);
     if (prof) t_wait += clock64() - tw0;
     const double* st = stages + s * kStage;
-    const double *AX = st, *AY = st + 1024, *BX = st + kTmaPanel, *BY = st + kTmaPanel + 1024;
+    const int tcur = first + (it >> lnk) * stride;
+    const bool dcur = (tcur >> lnt) == (tcur & (nt - 1));
+    const double *AX = st, *AY = st + 1024;
+    const double *BX = dcur ? AX : st + kTmaPanel, *BY = dcur ? AY : st + kTmaPanel + 1024;
 #pragma unroll
     for (int kb = 0; kb < KC; kb += 4) {
       double xa[2], ya[2], xn[2], xb[4], yb[4];
