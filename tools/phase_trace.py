@@ -1,9 +1,11 @@
-"""Per-phase cycle breakdown of the SMEM-tier anneal kernel (CTA 0, first replica).
+"""Per-phase cycle breakdown of the anneal kernel (CTA 0, first replica): the SMEM tier for
+spins <= 12, the HBM tier above (TG_HBM_CTAS_PER_REPLICA picks its cluster size).
 
     python tools/phase_trace.py [spins] [replicas] [steps]
 
 Stamps (clock64): 0 step start, 1 gate pass done, 2 GEMM done (partials posted),
-3 decision done.
+3 decision done; HBM tier also: GEMM-internal chunk waits, tile epilogues, and the
+largest per-warp wait (thread 0's view).
 """
 import os
 import sys
