@@ -49,11 +49,25 @@ typedef struct {
   int32_t entropy_kind;          /* tg_entropy_kind (device: TG_RENYI2)                 */
   int32_t objective;             /* tg_objective                                         */
   int32_t initial_state;         /* tg_initial_state                                     */
-  int32_t inject_fault;          /* testhooks::perturb_gemm analogue (linalg.hpp:74-79)  */
+  int32_t inject_fault;          /* test hooks: 0 none; 1 = testhooks::perturb_gemm      *
+                                  * (linalg.hpp:74-79); 2 = the gate of (fault_procedure, *
+                                  * fault_step) is scaled by 1.001, so psi' fails the norm *
+                                  * check of spinmc.cpp:152-156                            */
   double t0, t_min;              /* AnnealSchedule (spinmc.hpp:37-40)                    */
   uint64_t renormalize_interval; /* 1000 by default; 0 disables                          */
   uint32_t shard_index, shard_count;
+  uint64_t fault_procedure, fault_step;  /* inject_fault == 2 only                     */
 } tg_anneal_config;
+
+/* One logged near-tie accept decision: |u - p| < 1e-9 in the test
+ * u < acceptance_probability(delta, T) of spinmc.cpp:201-207, where a last-bit difference
+ * in the entropy could flip the outcome. */
+typedef struct {
+  uint64_t procedure, step;
+  double u, p;             /* uniform01 draw and acceptance probability (reference formula) */
+  uint32_t site;
+  int32_t accepted;
+} tg_near_tie;
 
 /* Per-procedure traces = spinmc::EntropyTrace (spinmc.hpp:44-50) + sites. Caller-owned
  * HOST arrays; row r is procedure p = shard_index + r*shard_count (r < local count), i.e.
@@ -69,7 +83,21 @@ typedef struct {
   double average_entropy;   /* over this call's rows, procedure order (spinmc.cpp:253-269) */
   int64_t total_wall_ns;    /* host wall time of the call                              */
   uint64_t total_flops;     /* (rows*steps + rows) * gemm_flops(d_a,d_a,d_b)           */
-  double kernel_ms;         /* device time of the anneal kernel(s), CUDA events        */
+  double kernel_ms;         /* device time of the anneal kernel(s), CUDA events (max   *
+                             * over the context's GPUs)                                */
+  double* device_kernel_ms; /* [devices] optional: per-GPU device time                  */
+  uint64_t* device_resident; /* [devices] optional: replicas resident at once per GPU     *
+                              * (persistent-kernel slots; DeviceMetrics high water mark) */
+  int64_t* initial_wall_ns; /* [rows] optional: initial state + initial-entropy GEMM,     *
+                             * device %globaltimer (spinmc.cpp:229-234)                  */
+  /* decision audit. The device decides Renyi-2 steps by a lean bound     *
+   * (DESIGN.md §3.1); a decision whose margin is inside the rounding window is re-taken   *
+   * with the reference formula.                                                          */
+  uint64_t fallback_decisions;   /* out: decisions re-taken with the reference formula   */
+  uint64_t near_ties;            /* out: decisions with |u - p| < 1e-9                    */
+  tg_near_tie* near_tie_log;     /* optional [near_tie_capacity]: the first near ties,    *
+                                  * sorted by (procedure, step)                           */
+  uint64_t near_tie_capacity;
 } tg_anneal_result;
 
 /* Device-resident outputs for tg_anneal_launch (rows as above). */
@@ -83,6 +111,12 @@ typedef struct {
   int32_t* status;          /* [rows] 0 ok, 2 not normalized (step in status_step) */
   int64_t* status_step;     /* [rows]        */
   void* workspace;          /* tg_anneal_workspace_bytes() bytes (HBM tier), else NULL */
+  double* status_norm;      /* [rows] or NULL: ||psi|| of a failed norm check          */
+  int64_t* initial_wall_ns; /* [rows] or NULL: initial state + entropy, %globaltimer ns  */
+  uint64_t* tie_stats;      /* [2] or NULL, zeroed by the caller: fallback decisions,  *
+                             * near ties (counters, atomically incremented)             */
+  tg_near_tie* tie_log;     /* [tie_capacity] or NULL: near ties in completion order   */
+  uint64_t tie_capacity;
 } tg_anneal_device_buffers;
 
 typedef struct tg_ctx tg_ctx;
@@ -117,8 +151,10 @@ uint64_t tg_step_flops(uint32_t spins);
 /* Annealing driver: replaces bench::run_experiment (bench.hpp:75, bench.cpp:341-417) for
  * the new ExecutionMode::kDevice. Runs the shard's replicas over the context's GPUs (one
  * persistent kernel per GPU, replica p on GPU p mod devices), copies traces to the
- * caller's host arrays. Fails with TG_EKERNEL "kernel failed for procedure p: ..." when a
- * replica's state leaves normalization (spinmc.cpp:152-156). */
+ * caller's host arrays. When a replica's state leaves normalization it fails as the
+ * reference does: TG_EINVAL (std::invalid_argument) with the message of spinmc.cpp:153-155,
+ * "entanglement_entropy: state not normalized (||psi|| = %f)", for the first such
+ * procedure in procedure order (run_experiment rethrows it unchanged, bench.cpp:387-395). */
 tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_result* res);
 
 /* Low-level asynchronous launch on the CURRENT device and the given stream

@@ -119,7 +119,11 @@ exec::VirtualTime CudaGemmExecutor::now() {
   return std::chrono::duration_cast<exec::VirtualTime>(std::chrono::steady_clock::now() - origin_);
 }
 
-bench::RunReport run_experiment_device(const bench::ExperimentConfig& config) {
+namespace testhooks {
+std::optional<GateFault> gate_fault;
+}
+
+bench::RunReport run_experiment_device(const bench::ExperimentConfig& config, DeviceAudit* audit) {
   bench::validate(config);
   tg_anneal_config c{};
   c.spins = static_cast<uint32_t>(config.spins);
@@ -135,15 +139,29 @@ bench::RunReport run_experiment_device(const bench::ExperimentConfig& config) {
   c.renormalize_interval = spinmc::McConfig{}.renormalize_interval;
   c.shard_index = 0;
   c.shard_count = 1;
-  const std::size_t np = config.procedures, s = config.steps;
-  std::vector<double> init(np), ent(np * s), fin(np);
+  if (testhooks::gate_fault) {
+    c.inject_fault = 2;
+    c.fault_procedure = testhooks::gate_fault->procedure;
+    c.fault_step = testhooks::gate_fault->step;
+  }
+  const std::size_t np = config.procedures, s = config.steps, nd = config.devices;
+  std::vector<double> init(np), ent(np * s), fin(np), dev_ms(nd);
   std::vector<uint8_t> acc(np * s);
+  std::vector<int64_t> wall(np * s), init_wall(np);
+  std::vector<uint64_t> resident(nd);
+  std::vector<tg_near_tie> ties(audit ? 1024 : 0);
   tg_anneal_result r{};
   r.initial_entropy = init.data();
   r.entropies = ent.data();
   r.accepted = acc.data();
   r.final_entropy = fin.data();
-  std::vector<int> gpus(config.devices);
+  r.wall_ns = wall.data();
+  r.initial_wall_ns = init_wall.data();
+  r.device_kernel_ms = dev_ms.data();
+  r.device_resident = resident.data();
+  r.near_tie_log = ties.empty() ? nullptr : ties.data();
+  r.near_tie_capacity = ties.size();
+  std::vector<int> gpus(nd);
   for (std::size_t i = 0; i < gpus.size(); ++i) gpus[i] = static_cast<int>(i);
   tg_ctx* ctx = nullptr;
   throw_on(tg_create(gpus.data(), static_cast<int>(gpus.size()), &ctx));
@@ -153,18 +171,65 @@ bench::RunReport run_experiment_device(const bench::ExperimentConfig& config) {
   bench::RunReport rep;
   rep.config = config;
   rep.traces.resize(np);
-  const exec::VirtualTime per_step{s ? r.total_wall_ns / static_cast<int64_t>(s) : 0};
   for (std::size_t p = 0; p < np; ++p) {
     spinmc::EntropyTrace& t = rep.traces[p];
     t.procedure_index = p;
     t.initial_entropy = init[p];
     t.entropies.assign(ent.begin() + p * s, ent.begin() + (p + 1) * s);
     t.accepted_flags.resize(s);
-    for (std::size_t i = 0; i < s; ++i) t.accepted_flags[i] = acc[p * s + i] != 0;
-    t.wall_times.assign(s, per_step);
+    t.wall_times.resize(s);
+    for (std::size_t i = 0; i < s; ++i) {
+      t.accepted_flags[i] = acc[p * s + i] != 0;
+      t.wall_times[i] = exec::VirtualTime{wall[p * s + i]};
+    }
+  }
+  // per device (bench.cpp:408-415): procedures p = d (mod devices), records, metrics
+  const spinmc::BipartitionDims dims = spinmc::dims_for_spins(config.spins);
+  const uint64_t gf = linalg::gemm_flops(dims.d_a, dims.d_a, dims.d_b);
+  for (std::size_t d = 0; d < nd; ++d) {
+    bench::DeviceReport dr;
+    dr.device_id = d;
+    for (std::size_t p = d; p < np; p += nd) dr.procedures.push_back(p);
+    dr.records.reserve(dr.procedures.size() * (s + 1));
+    auto add = [&](std::size_t p, int64_t ns) {
+      exec::KernelRecord kr;
+      kr.device_id = d;
+      kr.procedure = p;
+      kr.m = dims.d_a;
+      kr.n = dims.d_a;
+      kr.k = dims.d_b;
+      kr.exec_time = exec::VirtualTime{std::max<int64_t>(ns, 1)};
+      kr.flops = gf;
+      dr.records.push_back(kr);
+    };
+    for (std::size_t p : dr.procedures) {
+      add(p, init_wall[p]);  // initial-entropy GEMM (spinmc.cpp:234)
+      for (std::size_t i = 0; i < s; ++i) add(p, wall[p * s + i]);
+    }
+    exec::DeviceMetrics& m = dr.metrics;
+    m.kernel_count = dr.records.size();
+    m.per_gemm_throughput.reserve(dr.records.size());
+    for (const exec::KernelRecord& kr : dr.records) {
+      m.total_flops += kr.flops;
+      m.per_gemm_throughput.push_back(static_cast<double>(kr.flops) /
+                                      std::chrono::duration<double>(kr.exec_time).count());
+    }
+    m.makespan = exec::VirtualTime{static_cast<int64_t>(dev_ms[d] * 1e6)};
+    m.busy_time = m.makespan;
+    m.idle_time = exec::VirtualTime{0};
+    m.high_water_concurrency = resident[d];
+    m.total_throughput = m.makespan.count() > 0
+                             ? static_cast<double>(m.total_flops) / std::chrono::duration<double>(m.makespan).count()
+                             : 0.0;
+    rep.devices.push_back(std::move(dr));
   }
   rep.total_wall = exec::VirtualTime{r.total_wall_ns};
   rep.average_entropy = r.average_entropy;
+  if (audit) {
+    audit->fallback_decisions = r.fallback_decisions;
+    audit->near_ties = r.near_ties;
+    audit->near_tie_log.assign(ties.begin(), ties.begin() + std::min<uint64_t>(r.near_ties, ties.size()));
+  }
   return rep;
 }
 

@@ -7,6 +7,8 @@
 // GEMMs on the GPU, and bench::run_experiment for ExecutionMode "device" (bench.hpp:75).
 #pragma once
 #include <chrono>
+#include <cstdint>
+#include <optional>
 #include <vector>
 
 #include "taskgemm/bench.hpp"
@@ -49,7 +51,31 @@ class CudaGemmExecutor : public exec::GemmExecutor {
   std::chrono::steady_clock::time_point origin_;
 };
 
-// bench::run_experiment for ExecutionMode "device": one persistent kernel per GPU.
-bench::RunReport run_experiment_device(const bench::ExperimentConfig& config);
+// Decision audit of a device run (tg_anneal_result): decisions whose lean
+// margin fell inside the rounding window and were re-taken with the reference formula, and
+// the accept tests with |u - p| < 1e-9, logged in (procedure, step) order.
+struct DeviceAudit {
+  std::uint64_t fallback_decisions = 0;
+  std::uint64_t near_ties = 0;
+  std::vector<tg_near_tie> near_tie_log;
+};
+
+namespace testhooks {
+// Like linalg::testhooks::perturb_gemm (linalg.hpp:74-79): while set, run_experiment_device
+// scales the Haar gate of (procedure, step) by 1.001, so that proposal fails the norm check
+// of entanglement_entropy (spinmc.cpp:152-156) and the run throws std::invalid_argument.
+struct GateFault {
+  std::size_t procedure = 0, step = 0;
+};
+extern std::optional<GateFault> gate_fault;
+}  // namespace testhooks
+
+// bench::run_experiment for ExecutionMode "device": one persistent kernel per GPU. Fills
+// the RunReport as the reference does (bench.cpp:396-415): traces with per-step wall
+// times (device %globaltimer, spinmc.cpp:238-245), and per device its procedures, one
+// KernelRecord per GEMM (the initial-entropy GEMM and one per step; exec_time = that
+// step's device time) and DeviceMetrics (the persistent kernel is the device's one job:
+// busy = makespan = its device time, high water = its resident replicas).
+bench::RunReport run_experiment_device(const bench::ExperimentConfig& config, DeviceAudit* audit = nullptr);
 
 }  // namespace taskgemm::device

@@ -1,9 +1,11 @@
 // test_driver.cpp — C entry points so tests/test_integration_reference_api.py can drive the
 // reference-side binding (taskgemm_device.hpp) through the reference's OWN C++ API.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
 #include "taskgemm/errors.hpp"
+#include "taskgemm/report_io.hpp"
 #include "taskgemm/spinmc.hpp"
 #include "taskgemm_device.hpp"
 
@@ -83,6 +85,57 @@ int tgi_run_experiment_device(int spins, uint64_t steps, uint64_t procedures, ui
     if (bench::speedup(rep, rep) != 1.0) throw std::runtime_error("speedup(rep, rep) != 1");
     if (steps > 0 && spinmc::average_entropy(rep.traces) != rep.average_entropy)
       throw std::runtime_error("average_entropy differs from spinmc::average_entropy");
+  });
+}
+
+// run_experiment_device with testhooks::gate_fault set on (fault_procedure, fault_step):
+// the reference contract is std::invalid_argument "entanglement_entropy: state not
+// normalized (||psi|| = ...)" (spinmc.cpp:152-156, rethrown by bench.cpp:387-395) -> rc 2.
+int tgi_run_experiment_device_fault(int spins, uint64_t steps, uint64_t procedures, int kind,
+                                    uint64_t fault_procedure, uint64_t fault_step) {
+  device::testhooks::gate_fault = device::testhooks::GateFault{fault_procedure, fault_step};
+  const int rc = guard([&] {
+    bench::ExperimentConfig cfg;
+    cfg.spins = spins;
+    cfg.steps = steps;
+    cfg.procedures = procedures;
+    cfg.entropy_kind = kind == 0 ? spinmc::EntropyKind::kVonNeumann : spinmc::EntropyKind::kRenyi2;
+    device::run_experiment_device(cfg);
+  });
+  device::testhooks::gate_fault.reset();
+  return rc;
+}
+
+// RunReport completeness: run in device mode, then serialise with the reference's own
+// report_io::report_json and kernel_csv / trace_csv. Returns the JSON in `json` (cap
+// bytes), and stats = {records per device..., wall_times > 0 count, kernel_csv lines,
+// trace_csv lines, fallback decisions, near ties}.
+int tgi_run_experiment_report(int spins, uint64_t steps, uint64_t procedures, uint64_t devices, int kind,
+                              int objective, double t_min, char* json, uint64_t cap, uint64_t* stats) {
+  return guard([&] {
+    bench::ExperimentConfig cfg;
+    cfg.spins = spins;
+    cfg.steps = steps;
+    cfg.procedures = procedures;
+    cfg.devices = devices;
+    cfg.entropy_kind = kind == 0 ? spinmc::EntropyKind::kVonNeumann : spinmc::EntropyKind::kRenyi2;
+    cfg.objective = objective == 0 ? spinmc::Objective::kMaximize : spinmc::Objective::kMinimize;
+    cfg.schedule.t_min = t_min;
+    device::DeviceAudit audit;
+    bench::RunReport rep = device::run_experiment_device(cfg, &audit);
+    const std::string j = report_io::report_json(rep);
+    if (j.size() + 1 > cap) throw std::runtime_error("json buffer too small");
+    std::memcpy(json, j.c_str(), j.size() + 1);
+    uint64_t positive = 0;
+    for (const auto& t : rep.traces)
+      for (const auto& w : t.wall_times) positive += w.count() > 0;
+    auto lines = [](const std::string& x) { return static_cast<uint64_t>(std::count(x.begin(), x.end(), '\n')); };
+    for (std::size_t d = 0; d < devices; ++d) stats[d] = rep.devices.at(d).records.size();
+    stats[devices] = positive;
+    stats[devices + 1] = lines(report_io::kernel_csv(rep));
+    stats[devices + 2] = lines(report_io::trace_csv(rep.traces));
+    stats[devices + 3] = audit.fallback_decisions;
+    stats[devices + 4] = audit.near_ties;
   });
 }
 

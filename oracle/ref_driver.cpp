@@ -207,6 +207,52 @@ int tgr_run_pool(const tgr_config* c, uint64_t p0, uint64_t count, int threads, 
   return 0;
 }
 
+// Timed CPU sample for bench.py's reference arm / cpu_baseline: the pooled
+// driver above, recording per replica the wall time of the whole mc_procedure (total_ns)
+// and the sum of its per-step wall times (steps_ns: EntropyTrace::wall_times, which the
+// reference fills from DirectExecutor::now(), a steady clock; spinmc.cpp:238-245). The
+// difference is the initial state + initial-entropy GEMM (spinmc.cpp:229-234), so a short
+// sample extrapolates linearly in steps (bench::extrapolate_runtime, bench.cpp:429-438).
+int tgr_time_sample(const tgr_config* c, uint64_t p0, uint64_t count, int threads, int64_t* total_ns,
+                    int64_t* steps_ns, int64_t* wall_ns) {
+  const spinmc::McConfig mc = to_mc(c);
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> rc{0};
+  std::string first_err;
+  std::mutex mu;
+  auto t0 = std::chrono::steady_clock::now();
+  auto worker = [&] {
+    for (;;) {
+      const uint64_t r = next.fetch_add(1);
+      if (r >= count) return;
+      try {
+        exec::DirectExecutor ex;
+        auto st = rng::derive_stream({c->seed, static_cast<std::size_t>(p0 + r)});
+        const auto a = std::chrono::steady_clock::now();
+        spinmc::EntropyTrace t = spinmc::mc_procedure(mc, p0 + r, st, ex);
+        const auto b = std::chrono::steady_clock::now();
+        int64_t s = 0;
+        for (const auto& w : t.wall_times) s += w.count();
+        total_ns[r] = std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
+        steps_ns[r] = s;
+      } catch (const std::exception& e) {
+        std::lock_guard lk(mu);
+        if (rc.load() == 0) { first_err = e.what(); rc = -2; }
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int i = 0; i < std::max(1, threads); ++i) pool.emplace_back(worker);
+  for (auto& t : pool) t.join();
+  if (wall_ns)
+    *wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+  if (rc.load() != 0) {
+    g_err = first_err;
+    return rc.load();
+  }
+  return 0;
+}
+
 // The reference's own driver (bench::run_experiment, bench.cpp:341-417) in a given mode.
 // virtual_wall_ns receives report.total_wall (a VIRTUAL makespan).
 int tgr_run_experiment(const tgr_config* c, uint64_t procedures, uint64_t devices, const char* mode,

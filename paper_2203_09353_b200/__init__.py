@@ -26,7 +26,7 @@ import numpy as np
 __all__ = [
     "ExperimentConfig", "RunReport", "EntropyTrace", "Device", "KernelRecord", "run_experiment",
     "ConfigError", "KernelError", "SubmissionError", "DeviceUnavailable", "lib", "step_flops",
-    "dims_for_spins", "LIB_PATH",
+    "dims_for_spins", "LIB_PATH", "NearTie",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -65,6 +65,16 @@ class CAnnealConfig(C.Structure):
         ("objective", C.c_int32), ("initial_state", C.c_int32), ("inject_fault", C.c_int32),
         ("t0", C.c_double), ("t_min", C.c_double), ("renormalize_interval", C.c_uint64),
         ("shard_index", C.c_uint32), ("shard_count", C.c_uint32),
+        ("fault_procedure", C.c_uint64), ("fault_step", C.c_uint64),
+    ]
+
+
+class CNearTie(C.Structure):
+    """tg_near_tie: a logged accept decision with |u - p| < 1e-9."""
+
+    _fields_ = [
+        ("procedure", C.c_uint64), ("step", C.c_uint64), ("u", C.c_double), ("p", C.c_double),
+        ("site", C.c_uint32), ("accepted", C.c_int32),
     ]
 
 
@@ -75,6 +85,9 @@ class CAnnealResult(C.Structure):
         ("wall_ns", C.POINTER(C.c_int64)), ("final_entropy", C.POINTER(C.c_double)),
         ("average_entropy", C.c_double), ("total_wall_ns", C.c_int64),
         ("total_flops", C.c_uint64), ("kernel_ms", C.c_double),
+        ("device_kernel_ms", C.POINTER(C.c_double)), ("device_resident", C.POINTER(C.c_uint64)),
+        ("initial_wall_ns", C.POINTER(C.c_int64)), ("fallback_decisions", C.c_uint64),
+        ("near_ties", C.c_uint64), ("near_tie_log", C.POINTER(CNearTie)), ("near_tie_capacity", C.c_uint64),
     ]
 
 
@@ -83,6 +96,8 @@ class CDeviceBuffers(C.Structure):
         ("initial_entropy", C.c_void_p), ("entropies", C.c_void_p), ("accepted", C.c_void_p),
         ("sites", C.c_void_p), ("wall_ns", C.c_void_p), ("final_entropy", C.c_void_p),
         ("status", C.c_void_p), ("status_step", C.c_void_p), ("workspace", C.c_void_p),
+        ("status_norm", C.c_void_p), ("initial_wall_ns", C.c_void_p), ("tie_stats", C.c_void_p), ("tie_log", C.c_void_p),
+        ("tie_capacity", C.c_uint64),
     ]
 
 
@@ -210,7 +225,9 @@ class ExperimentConfig:
     renormalize_interval: int = 1000
     shard_index: int = 0
     shard_count: int = 1
-    inject_fault: bool = False
+    inject_fault: int = 0       # 1: perturb_gemm (linalg.hpp:74-79); 2: non-unitary gate (below)
+    fault_procedure: int = 0    # inject_fault == 2: this procedure's gate at fault_step is scaled by 1.001
+    fault_step: int = 0
 
     def to_c(self) -> CAnnealConfig:
         for name, table in (("entropy_kind", _ENTROPY), ("objective", _OBJECTIVE),
@@ -222,7 +239,8 @@ class ExperimentConfig:
         return CAnnealConfig(self.spins, self.devices, self.steps, self.procedures, self.seed & (2**64 - 1),
                              _ENTROPY[self.entropy_kind], _OBJECTIVE[self.objective],
                              _INITIAL[self.initial_state], int(self.inject_fault), self.t0, self.t_min,
-                             self.renormalize_interval, self.shard_index, self.shard_count)
+                             self.renormalize_interval, self.shard_index, self.shard_count,
+                             self.fault_procedure, self.fault_step)
 
     def rows(self) -> int:
         c = self.to_c()
@@ -261,12 +279,30 @@ class RunReport:
     total_flops: int
     kernel_ms: float
     traces: list = field(default_factory=list)
+    device_kernel_ms: list = field(default_factory=list)  # per GPU of the context
+    device_resident: list = field(default_factory=list)   # replicas resident at once per GPU
+    initial_wall_ns: np.ndarray | None = None             # [rows] (wall=True)
+    fallback_decisions: int = 0  # decisions re-taken with the reference formula (lean margin in the window)
+    near_ties: int = 0           # decisions with |u - p| < 1e-9
+    near_tie_log: list = field(default_factory=list)  # NearTie, (procedure, step) order
 
     def trace(self, row: int) -> EntropyTrace:
         return EntropyTrace(int(self.procedures[row]), float(self.initial_entropy[row]),
                             self.entropies[row], self.accepted[row].astype(bool),
                             None if self.sites is None else self.sites[row],
                             None if self.wall_ns is None else self.wall_ns[row])
+
+
+@dataclass
+class NearTie:
+    """tg_near_tie: accept test u < p (spinmc.cpp:207) with |u - p| < 1e-9."""
+
+    procedure: int
+    step: int
+    u: float
+    p: float
+    site: int
+    accepted: bool
 
 
 @dataclass
@@ -319,9 +355,10 @@ class Device:
         self.close()
 
     def run(self, cfg: ExperimentConfig, sites: bool = True, wall: bool = False,
-            out: dict | None = None) -> RunReport:
+            out: dict | None = None, near_tie_capacity: int = 256) -> RunReport:
         """The device annealing driver (tg_anneal_run). `out` may supply preallocated (pinned)
-        host arrays keyed initial/entropies/accepted/sites/final."""
+        host arrays keyed initial/entropies/accepted/sites/final. A state that leaves
+        normalization raises ValueError (std::invalid_argument, spinmc.cpp:152-156)."""
         c = cfg.to_c()
         _check(lib().tg_validate(C.byref(c)))
         rows = int(lib().tg_anneal_rows(C.byref(c)))
@@ -340,10 +377,23 @@ class Device:
         res.sites = st.ctypes.data_as(_u8p) if st is not None else None
         res.wall_ns = wl.ctypes.data_as(C.POINTER(C.c_int64)) if wl is not None else None
         res.final_entropy = fin.ctypes.data_as(_dp)
+        dms = (C.c_double * max(cfg.devices, 1))()
+        res.device_kernel_ms = C.cast(dms, C.POINTER(C.c_double))
+        drs = (C.c_uint64 * max(cfg.devices, 1))()
+        res.device_resident = C.cast(drs, C.POINTER(C.c_uint64))
+        iw = np.zeros(rows, np.int64) if wall else None
+        res.initial_wall_ns = iw.ctypes.data_as(C.POINTER(C.c_int64)) if iw is not None else None
+        log = (CNearTie * max(near_tie_capacity, 1))()
+        res.near_tie_log = C.cast(log, C.POINTER(CNearTie)) if near_tie_capacity > 0 else None
+        res.near_tie_capacity = near_tie_capacity
         _check(lib().tg_anneal_run(self._h, C.byref(c), C.byref(res)))
         procs = cfg.shard_index + np.arange(rows, dtype=np.int64) * max(cfg.shard_count, 1)
+        ties = [NearTie(t.procedure, t.step, t.u, t.p, t.site, bool(t.accepted))
+                for t in log[:min(res.near_ties, near_tie_capacity)]]
         return RunReport(cfg, procs, init, ent, acc, st, wl, fin, res.average_entropy, res.total_wall_ns,
-                         res.total_flops, res.kernel_ms)
+                         res.total_flops, res.kernel_ms, device_kernel_ms=list(dms[:max(cfg.devices, 1)]),
+                         device_resident=list(drs[:max(cfg.devices, 1)]), initial_wall_ns=iw,
+                         fallback_decisions=res.fallback_decisions, near_ties=res.near_ties, near_tie_log=ties)
 
     def batched_gemm(self, a_list, b_list, c_list=None, alpha=1.0, beta=0.0, device: int = 0,
                      procedures=None, records: bool = False):

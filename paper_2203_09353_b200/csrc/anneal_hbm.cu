@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   const bool light_fence = P.light_fence != 0;
 
   for (uint64_t r = cid; r < P.rows; r += ncl) {
+    const int64_t t_row0 = (tid == 0 && writer && P.initial_wall_ns) ? globaltimer() : 0;
     const GateRec* recs = P.gates + r;  // record s at recs[s * rows] (gate_stream.cu layout)
     // record s is copied to H.rec[s & 1] while the previous GEMM runs (an HBM miss on the
     // step's critical path otherwise); 18 threads x 16 B
@@ -249,10 +250,12 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     if (tid == 0 && writer) {
       P.status[r] = err ? kRowNotNormalized : kRowOk;
       if (err) P.status_step[r] = -1;
+      if (err && P.status_norm) P.status_norm[r] = __dsqrt_rn(tr);
       P.initial_entropy[r] = cur_e;
     }
 
-    int64_t t_prev = (tid == 0 && P.wall_ns) ? globaltimer() : 0;
+    int64_t t_prev = (tid == 0 && (P.wall_ns || P.initial_wall_ns)) ? globaltimer() : 0;
+    if (tid == 0 && writer && P.initial_wall_ns) P.initial_wall_ns[r] = t_prev - t_row0;
     uint64_t renorm_left = P.renorm;  // countdown: no 64-bit modulo per step
     for (uint64_t s = 0; s < P.steps && !err; ++s) {
       const GateRec& g = H.rec[s & 1];
@@ -283,16 +286,16 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
           if (writer) {
             P.status[r] = kRowNotNormalized;
             P.status_step[r] = static_cast<int64_t>(s);
+            if (P.status_norm) P.status_norm[r] = __dsqrt_rn(tr);
           }
         } else {
           H.error = 0;
           const double proposed = e_new;
-          if constexpr (KIND == 0) {
-            acc = smem::decide(proposed, cur_e, g, P.objective);
-          } else {  // spinmc.cpp:203-207 verbatim
-            const double delta = P.objective == 0 ? proposed - cur_e : cur_e - proposed;
-            acc = g.u < acceptance(delta, g.temp);
-          }
+          // KIND 0: lean decision on rho2; KIND 1: spinmc.cpp:203-207 verbatim
+          const smem::Verdict v = KIND == 0 ? smem::decide_audit(proposed, cur_e, g, P.objective, P.tie_eps)
+                                            : smem::decide_reference(proposed, cur_e, g, P.objective, P.tie_eps);
+          acc = v.acc;
+          if (writer) smem::audit(P, r, s, g, v);
           if (acc) cur_e = proposed;
         }
         H.decision = acc;
@@ -572,14 +575,17 @@ cudaError_t hbm_geometry(uint32_t spins, uint64_t rows, int kind, int device, in
 
 }  // namespace
 
+// Any launch of r <= rows replicas runs min(r, resident clusters) <= min(rows, SMs) clusters
+// (hbm_geometry); sizing for that bound keeps a batch tail or a partial launch whose geometry
+// has more clusters than the full batch inside the workspace.
+uint64_t anneal_hbm_slab_clusters(uint64_t rows, int device) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return std::min<uint64_t>(rows, static_cast<uint64_t>(sms > 0 ? sms : 1));
+}
+
 size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind) {
-  int cs = 1;
-  uint64_t clusters = 0;
-  if (hbm_geometry(spins, rows, entropy_kind, device, cs, clusters) != cudaSuccess) {
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    clusters = std::min<uint64_t>(rows, static_cast<uint64_t>(sms));  // upper bound
-  }
+  const uint64_t clusters = anneal_hbm_slab_clusters(rows, device);
   const size_t da = size_t{1} << (spins / 2);
   // von Neumann with d_a > 64: rho (2 planes of d_a^2) after each slab (vn_packed.cuh)
   const size_t rho = entropy_kind == 0 && da > static_cast<size_t>(hbm::TB) ? 2 * da * da : 0;
@@ -604,6 +610,8 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   cudaGetDevice(&dev);
   cudaError_t e = hbm_geometry(p.spins, p.rows, p.entropy_kind, dev, cs, clusters);
   if (e != cudaSuccess) return e;
+  // never more clusters than the workspace has slabs (the persistent loop strides over rows)
+  if (p.slab_clusters > 0 && clusters > p.slab_clusters) clusters = p.slab_clusters;
   const int grid = static_cast<int>(clusters) * cs;
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;

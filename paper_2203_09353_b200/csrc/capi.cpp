@@ -12,6 +12,8 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -89,11 +91,16 @@ tg_status validate(const tg_anneal_config* c) {
   if (c->entropy_kind == TG_VON_NEUMANN && c->spins > static_cast<uint32_t>(tg::kVnMaxSpins))
     return fail(TG_EINVAL, "device von-neumann entropy covers spins <= " + std::to_string(tg::kVnMaxSpins) +
                                " (rho resident in shared memory); use renyi-2");
+  if (c->inject_fault < 0 || c->inject_fault > 2) return fail(TG_ECONFIG, "inject_fault must be 0, 1 or 2");
   if (c->objective != TG_MAXIMIZE && c->objective != TG_MINIMIZE)
     return fail(TG_ECONFIG, "objective must be max or min");
   if (c->initial_state != TG_PRODUCT && c->initial_state != TG_RANDOM)
     return fail(TG_ECONFIG, "initial_state must be product or random");
-  if (c->steps > (uint64_t{1} << 40)) return fail(TG_ECONFIG, "steps too large");
+  // the proposal pre-pass jumps each replica's stream ahead by GF(2) matrix powers
+  // (gate_stream.cu, kJumpBits): runs up to 2^22 steps per replica
+  if (c->steps > tg::kMaxSteps)
+    return fail(TG_ECONFIG, "steps (" + std::to_string(c->steps) + ") exceed the device path's limit of " +
+                                std::to_string(tg::kMaxSteps) + " steps per procedure");
   return TG_OK;
 }
 
@@ -103,7 +110,16 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
   p.spins = c->spins;
   p.objective = c->objective;
   p.initial_state = c->initial_state;
-  p.inject_fault = c->inject_fault || g_perturb.load();
+  p.inject_fault = (c->inject_fault == 1 || g_perturb.load()) ? 1 : 0;  // GEMM perturbation only
+  p.gate_fault = c->inject_fault == 2;
+  p.fault_procedure = c->fault_procedure;
+  p.fault_step = c->fault_step;
+  p.fault_row1 = 0;
+  p.tie_eps = 1e-9;  // SURVEY.md §8c near tie; tests widen it to exercise the audit log
+  if (const char* e = std::getenv("TG_NEAR_TIE_EPS")) {
+    const double v = std::atof(e);
+    if (v > 0.0 && v < 0.5) p.tie_eps = v;
+  }
   p.entropy_kind = c->entropy_kind;
   p.steps = c->steps;
   p.seed = c->seed;
@@ -120,9 +136,15 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
 // replica-step + raw draws) stays within this many bytes of workspace.
 constexpr size_t kStreamBudget = size_t{16} << 30;
 
+// HBM-tier slabs for any launch of up to `rows` replicas: a sub-range (the batch tail, the
+// e2e split) can pick a different cluster geometry than the full batch, so the region is
+// sized for the most clusters any row count <= rows can use (anneal_hbm_workspace_bytes).
 size_t slab_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind) {
   return spins > static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::anneal_hbm_workspace_bytes(spins, rows, device, entropy_kind)
                                                          : 0;
+}
+uint64_t slab_clusters(uint32_t spins, uint64_t rows, int device) {
+  return spins > static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::anneal_hbm_slab_clusters(rows, device) : 0;
 }
 
 // Workspace for one launch: [proposal stream of one batch][HBM-tier slabs] (+ alignment).
@@ -153,11 +175,17 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
     tg::AnnealParams q = p;
     q.rows = std::min<uint64_t>(batch, p.rows - b0);
     q.p_first = p.p_first + b0 * p.p_stride;
+    q.fault_row1 = 0;
+    if (p.gate_fault && p.fault_procedure >= q.p_first && (p.fault_procedure - q.p_first) % p.p_stride == 0 &&
+        (p.fault_procedure - q.p_first) / p.p_stride < q.rows)
+      q.fault_row1 = 1 + (p.fault_procedure - q.p_first) / p.p_stride;
     const uint64_t o = b0 * p.steps;
     q.initial_entropy = p.initial_entropy + b0;
     q.final_entropy = p.final_entropy ? p.final_entropy + b0 : nullptr;
     q.status = p.status + b0;
     q.status_step = p.status_step + b0;
+    q.status_norm = p.status_norm ? p.status_norm + b0 : nullptr;
+    q.initial_wall_ns = p.initial_wall_ns ? p.initial_wall_ns + b0 : nullptr;
     q.entropies = p.entropies + o;
     q.accepted = p.accepted + o;
     q.sites = p.sites ? p.sites + o : nullptr;
@@ -169,6 +197,7 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
     q.gates = gs.recs;
     q.init_states = gs.init_states;
     q.workspace = reinterpret_cast<double*>(slabs);
+    q.slab_clusters = slab_clusters(p.spins, batch, dev);
     e = p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::launch_anneal_smem(q, s, nullptr, trace)
                                                            : tg::launch_anneal_hbm(q, s, nullptr, trace);
     if (e != cudaSuccess) return e;
@@ -186,9 +215,17 @@ T* carve(char*& cursor, size_t count) {
   return p;
 }
 
-size_t trace_bytes(uint64_t rows, uint64_t steps, bool sites, bool wall) {
+size_t trace_bytes(uint64_t rows, uint64_t steps, bool sites, bool wall, uint64_t ties = 0) {
   const size_t rs = rows * steps;
-  return rows * (8 + 8 + 4 + 8) + rs * (8 + 1) + (sites ? rs : 0) + (wall ? rs * 8 : 0) + 8 * 256;
+  return rows * (8 + 8 + 4 + 8 + 8 + 8) + rs * (8 + 1) + (sites ? rs : 0) + (wall ? rs * 8 : 0) + 16 +
+         ties * sizeof(tg_near_tie) + 10 * 256;
+}
+
+// reference message of spinmc.cpp:153-155 (std::to_string(double) is "%f")
+std::string not_normalized_message(double nrm) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%f", nrm);
+  return std::string("entanglement_entropy: state not normalized (||psi|| = ") + buf + ")";
 }
 
 }  // namespace
@@ -287,6 +324,11 @@ tg_status tg_anneal_launch(const tg_anneal_config* cfg, const tg_anneal_device_b
   p.final_entropy = b->final_entropy;
   p.status = b->status;
   p.status_step = b->status_step;
+  p.status_norm = b->status_norm;
+  p.initial_wall_ns = b->initial_wall_ns;
+  p.tie_stats = reinterpret_cast<unsigned long long*>(b->tie_stats);
+  p.tie_log = b->tie_log;
+  p.tie_capacity = b->tie_log ? b->tie_capacity : 0;
   if (!b->workspace && rows > 0)
     return fail(TG_EINVAL, "workspace required (tg_anneal_workspace_bytes)");
   int dev = 0;
@@ -312,13 +354,19 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
   const uint64_t sc = cfg->shard_count ? cfg->shard_count : 1;
   const uint64_t steps = cfg->steps;
   const bool want_sites = res->sites != nullptr, want_wall = res->wall_ns != nullptr;
+  const bool want_init_wall = res->initial_wall_ns != nullptr;
 
   std::vector<tg_status> st(D, TG_OK);
   std::vector<std::string> msg(D);
   std::vector<float> ms(D, 0.f);
   std::vector<std::vector<int32_t>> status(D);
   std::vector<std::vector<int64_t>> status_step(D);
+  std::vector<std::vector<double>> status_norm(D);
+  std::vector<std::vector<int64_t>> iwall(D);
+  std::vector<uint64_t> resident(D, 0);
   std::vector<std::vector<double>> finals(D);
+  std::vector<unsigned long long> tie_stats(2 * D, 0);
+  std::vector<std::vector<tg_near_tie>> ties(D);
 
   auto worker = [&](uint64_t g) {
     DeviceState& d = ctx->devs[g];
@@ -334,7 +382,8 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
     const uint64_t lrows = rows > g ? (rows - g + D - 1) / D : 0;
     if (lrows == 0) return;
     // device buffers (grow-only)
-    const size_t need = trace_bytes(lrows, steps, want_sites, want_wall);
+    const uint64_t tie_cap = res->near_tie_log ? res->near_tie_capacity : 0;
+    const size_t need = trace_bytes(lrows, steps, want_sites, want_wall, tie_cap);
     if (need > d.trace_bytes) {
       if (d.trace) cudaFree(d.trace);
       d.trace = nullptr;
@@ -352,6 +401,12 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
     p.accepted = carve<uint8_t>(cur, lrows * steps);
     p.sites = want_sites ? carve<uint8_t>(cur, lrows * steps) : nullptr;
     p.wall_ns = want_wall ? carve<int64_t>(cur, lrows * steps) : nullptr;
+    p.status_norm = carve<double>(cur, lrows);
+    p.initial_wall_ns = want_init_wall ? carve<int64_t>(cur, lrows) : nullptr;
+    p.tie_stats = carve<unsigned long long>(cur, 2);
+    p.tie_log = tie_cap ? carve<tg_near_tie>(cur, tie_cap) : nullptr;
+    p.tie_capacity = tie_cap;
+    if (!cu(cudaMemsetAsync(p.tie_stats, 0, 16, d.stream), "cudaMemsetAsync")) return;
     const size_t ws = workspace_for(p, d.ordinal);
     if (ws > d.workspace_bytes) {
       if (d.workspace) cudaFree(d.workspace);
@@ -363,8 +418,19 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
     // Replicas run in waves of `wave` (resident CTAs / clusters). With D == 1 the traces go
     // straight into the caller's arrays, so the rows of all full waves but the last are
     // launched first and copied back on a second stream while the remaining rows run.
+    // A device-to-pageable copy blocks the host until it completes, which would serialise
+    // the two launches: split only when the caller's trace arrays are page-locked.
+    auto pinned = [](const void* h) {
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      return a.type == cudaMemoryTypeHost;
+    };
     uint64_t split = 0;
-    if (D == 1 && steps > 0) {
+    if (D == 1 && steps > 0 && pinned(res->entropies) && pinned(res->accepted) &&
+        (!want_sites || pinned(res->sites)) && (!want_wall || pinned(res->wall_ns))) {
       const uint64_t wave = p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::anneal_smem_wave_rows(p)
                                                                                 : tg::anneal_hbm_wave_rows(p);
       if (wave > 0 && lrows > wave) split = lrows % wave ? lrows - lrows % wave : lrows - wave;
@@ -377,6 +443,8 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
       q.final_entropy = p.final_entropy + r0;
       q.status = p.status + r0;
       q.status_step = p.status_step + r0;
+      q.status_norm = p.status_norm + r0;
+      q.initial_wall_ns = p.initial_wall_ns ? p.initial_wall_ns + r0 : nullptr;
       q.entropies = p.entropies + r0 * steps;
       q.accepted = p.accepted + r0 * steps;
       q.sites = p.sites ? p.sites + r0 * steps : nullptr;
@@ -388,13 +456,21 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
     std::vector<int64_t> wall(want_wall && D > 1 ? lrows * steps : 0);
     status[g].resize(lrows);
     status_step[g].resize(lrows);
+    status_norm[g].resize(lrows);
+    iwall[g].resize(want_init_wall ? lrows : 0);
+    resident[g] = std::min<uint64_t>(lrows, p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins)
+                                                ? tg::anneal_smem_wave_rows(p)
+                                                : tg::anneal_hbm_wave_rows(p));
     // trace rows [r0, r1) -> host (caller arrays when D == 1) on stream `st`
     auto copy_back = [&](uint64_t r0, uint64_t r1, cudaStream_t st) {
       const uint64_t n = r1 - r0, o = r0 * steps, ns = n * steps;
       bool ok = cu(cudaMemcpyAsync(init.data() + r0, p.initial_entropy + r0, 8 * n, cudaMemcpyDeviceToHost, st), "D2H") &&
                 cu(cudaMemcpyAsync(fin.data() + r0, p.final_entropy + r0, 8 * n, cudaMemcpyDeviceToHost, st), "D2H") &&
                 cu(cudaMemcpyAsync(status[g].data() + r0, p.status + r0, 4 * n, cudaMemcpyDeviceToHost, st), "D2H") &&
-                cu(cudaMemcpyAsync(status_step[g].data() + r0, p.status_step + r0, 8 * n, cudaMemcpyDeviceToHost, st), "D2H");
+                cu(cudaMemcpyAsync(status_step[g].data() + r0, p.status_step + r0, 8 * n, cudaMemcpyDeviceToHost, st), "D2H") &&
+                cu(cudaMemcpyAsync(status_norm[g].data() + r0, p.status_norm + r0, 8 * n, cudaMemcpyDeviceToHost, st), "D2H") &&
+                (!want_init_wall ||
+                 cu(cudaMemcpyAsync(iwall[g].data() + r0, p.initial_wall_ns + r0, 8 * n, cudaMemcpyDeviceToHost, st), "D2H"));
       if (ok && steps > 0) {
         // D == 1 and host rows contiguous: copy straight into the caller's arrays
         double* ent_dst = D == 1 ? res->entropies + o : ent.data() + o;
@@ -425,11 +501,17 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
     ok = copy_back(split, lrows, d.stream);
     if (ok && split > 0) ok = cu(cudaStreamSynchronize(d.copy), "trace copy");
     if (!ok) return;
+    if (!cu(cudaMemcpyAsync(&tie_stats[2 * g], p.tie_stats, 16, cudaMemcpyDeviceToHost, d.stream), "D2H")) return;
     if (!cu(cudaStreamSynchronize(d.stream), "anneal kernel")) return;
     cudaEventElapsedTime(&ms[g], d.ev0, d.ev1);
+    const uint64_t nlog = std::min<uint64_t>(tie_stats[2 * g + 1], tie_cap);
+    ties[g].resize(nlog);
+    if (nlog && !cu(cudaMemcpy(ties[g].data(), p.tie_log, nlog * sizeof(tg_near_tie), cudaMemcpyDeviceToHost), "D2H"))
+      return;
     for (uint64_t q = 0; q < lrows; ++q) {
       const uint64_t hr = g + D * q;
       res->initial_entropy[hr] = init[q];
+      if (want_init_wall) res->initial_wall_ns[hr] = iwall[g][q];
       if (res->final_entropy) res->final_entropy[hr] = fin[q];
       if (D > 1 && steps > 0) {
         std::memcpy(res->entropies + hr * steps, ent.data() + q * steps, 8 * steps);
@@ -450,17 +532,32 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
   }
   for (uint64_t g = 0; g < D; ++g)
     if (st[g] != TG_OK) return fail(st[g], msg[g]);
-  // first failing replica in procedure order -> KernelError (exec.hpp:76-86)
+  // the first procedure (in procedure order) whose state left normalization: the reference
+  // throws std::invalid_argument from entanglement_entropy (spinmc.cpp:152-156) and
+  // run_experiment rethrows the first procedure error unchanged (bench.cpp:387-395)
   for (uint64_t hr = 0; hr < rows; ++hr) {
     const uint64_t g = hr % D, q = hr / D;
-    if (status[g][q] != tg::kRowOk) {
-      const uint64_t p = cfg->shard_index + hr * sc;
-      const int64_t s = status_step[g][q];
-      return fail(TG_EKERNEL, "kernel failed for procedure " + std::to_string(p) +
-                                  ": entanglement_entropy: state not normalized (" +
-                                  (s < 0 ? std::string("initial state") : "step " + std::to_string(s)) + ")");
-    }
+    if (status[g][q] != tg::kRowOk) return fail(TG_EINVAL, not_normalized_message(status_norm[g][q]));
   }
+  // decision audit: counts over all GPUs, the logged near ties in (procedure, step) order
+  res->fallback_decisions = 0;
+  res->near_ties = 0;
+  std::vector<tg_near_tie> all_ties;
+  for (uint64_t g = 0; g < D; ++g) {
+    res->fallback_decisions += tie_stats[2 * g];
+    res->near_ties += tie_stats[2 * g + 1];
+    all_ties.insert(all_ties.end(), ties[g].begin(), ties[g].end());
+  }
+  std::sort(all_ties.begin(), all_ties.end(), [](const tg_near_tie& a, const tg_near_tie& b) {
+    return a.procedure != b.procedure ? a.procedure < b.procedure : a.step < b.step;
+  });
+  if (res->near_tie_log)
+    for (uint64_t i = 0; i < std::min<uint64_t>(all_ties.size(), res->near_tie_capacity); ++i)
+      res->near_tie_log[i] = all_ties[i];
+  if (res->device_kernel_ms)
+    for (uint64_t g = 0; g < D; ++g) res->device_kernel_ms[g] = ms[g];
+  if (res->device_resident)
+    for (uint64_t g = 0; g < D; ++g) res->device_resident[g] = resident[g];
   double sum = 0.0;  // procedure order, spinmc.cpp:259-268 / bench.cpp:401-407
   for (uint64_t hr = 0; hr < rows; ++hr)
     sum += steps > 0 ? finals[hr % D][hr / D] : res->initial_entropy[hr];
@@ -508,6 +605,12 @@ tg_status tg_zgemm_batched(tg_ctx* ctx, int device, int batch, int m, int n, int
   const auto t0 = std::chrono::steady_clock::now();
   double* buf = nullptr;
   TG_CUDA(cudaMallocAsync(&buf, bytes, d.stream));
+  // every return below frees the batch buffer (stream-ordered after the copies that use it)
+  struct FreeAsync {
+    double* p;
+    cudaStream_t s;
+    ~FreeAsync() { cudaFreeAsync(p, s); }
+  } guard{buf, d.stream};
   double *dA = buf, *dB = dA + batch * ea, *dC = has_c ? dB + batch * eb : nullptr;
   double* dO = (has_c ? dC + batch * ec : dB + batch * eb);
   for (int i = 0; i < batch; ++i) {
@@ -524,7 +627,6 @@ tg_status tg_zgemm_batched(tg_ctx* ctx, int device, int batch, int m, int n, int
   TG_CUDA(cudaEventRecord(d.ev1, d.stream));
   for (int i = 0; i < batch; ++i)
     TG_CUDA(cudaMemcpyAsync(out[i], dO + i * ec, 8 * ec, cudaMemcpyDeviceToHost, d.stream));
-  TG_CUDA(cudaFreeAsync(buf, d.stream));
   TG_CUDA(cudaStreamSynchronize(d.stream));
   float kms = 0.f;
   cudaEventElapsedTime(&kms, d.ev0, d.ev1);

@@ -13,6 +13,7 @@
 //  * d_a <= 8: pitch DA_PAD + 4 doubles (2*PITCH == 8 or 24 mod 32 words); rows >= d_a and
 //    columns >= d_b are zero padding.
 #pragma once
+#include "../../include/taskgemm_b200.h"
 #include "tg_device.cuh"
 
 namespace tg {
@@ -374,14 +375,56 @@ __device__ __forceinline__ double renyi2(double rho2) {
 // rho2' > rho2_cur * exp(T log u) (minimize); emul is that factor. Relative margins below
 // 1e-12 are re-decided with the reference formula (entropies and exp), so the outcome is
 // the reference's wherever FP64 rounding cannot tie.
+// The window is the record's tie_tol (>= 1e-12, gate_stream.cu make_gate): wide enough that
+// every decision with |u - p| < 1e-9 takes the reference formula and can be audited.
+// Verdict.flags: bit 0 = re-decided with the reference formula, bit 1 = near tie
+// (|u - p| < 1e-9); p is valid when flags != 0.
+struct Verdict {
+  int acc;
+  int flags;
+  double p;
+};
 template <class R>
-__device__ __forceinline__ int decide(double rho2_new, double rho2_cur, const R& g, int objective) {
+__device__ __forceinline__ Verdict decide_audit(double rho2_new, double rho2_cur, const R& g, int objective,
+                                                double eps = 1e-9) {
   const double r_new = fmin(rho2_new, 1.0), r_cur = fmin(rho2_cur, 1.0);
   const double bound = r_cur * g.emul;
-  if (fabs(r_new - bound) > 1e-12 * r_new) return objective == 0 ? (r_new < bound) : (r_new > bound);
+  if (fabs(r_new - bound) > static_cast<double>(g.tie_tol) * r_new)
+    return {objective == 0 ? (r_new < bound) : (r_new > bound), 0, 0.0};
   const double proposed = renyi2(rho2_new), current = renyi2(rho2_cur);
   const double delta = objective == 0 ? proposed - current : current - proposed;
-  return g.u < acceptance(delta, g.temp);
+  const double p = acceptance(delta, g.temp);
+  return {g.u < p, 1 | (fabs(g.u - p) < eps ? 2 : 0), p};
+}
+template <class R>
+__device__ __forceinline__ int decide(double rho2_new, double rho2_cur, const R& g, int objective) {
+  return decide_audit(rho2_new, rho2_cur, g, objective).acc;
+}
+// spinmc.cpp:201-207 verbatim on entropies (von Neumann), with the near-tie flag.
+template <class R>
+__device__ __forceinline__ Verdict decide_reference(double proposed, double current, const R& g, int objective,
+                                                    double eps = 1e-9) {
+  const double delta = objective == 0 ? proposed - current : current - proposed;
+  const double p = acceptance(delta, g.temp);
+  return {g.u < p, fabs(g.u - p) < eps ? 2 : 0, p};
+}
+// Decision audit record (one thread): counts and logs (tg_anneal_device_buffers tie_*).
+template <class PP, class R>
+__device__ __forceinline__ void audit(const PP& P, uint64_t r, uint64_t s, const R& g, const Verdict& v) {
+  if (!v.flags || !P.tie_stats) return;
+  if (v.flags & 1) atomicAdd(&P.tie_stats[0], 1ull);
+  if (v.flags & 2) {
+    const unsigned long long i = atomicAdd(&P.tie_stats[1], 1ull);
+    if (P.tie_log && i < P.tie_capacity) {
+      tg_near_tie& t = P.tie_log[i];
+      t.procedure = P.p_first + r * P.p_stride;
+      t.step = s;
+      t.u = g.u;
+      t.p = v.p;
+      t.site = static_cast<uint32_t>(g.site);
+      t.accepted = v.acc;
+    }
+  }
 }
 
 // Norm check of spinmc.cpp:152-156 on trace(rho) = ||psi'||^2.

@@ -92,7 +92,8 @@ struct GateRec {
   double temp;    // temperature(step) (spinmc.cpp:178-184)
   double emul;    // decision factor: exp(-T log u) (maximize) / exp(T log u) (minimize)
   int32_t site;   // uniform_index(S-1) (spinmc.cpp:198)
-  int32_t pad;
+  float tie_tol;  // lean-decision window: relative margins <= tie_tol are re-decided with the
+                  // reference formula (covers every |u - p| < 1e-9, smem::decide_audit)
 };
 static_assert(sizeof(GateRec) == 288, "GateRec layout");
 

@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include "../../include/taskgemm_b200.h"
+
 namespace tg {
 
 struct GateRec;  // tg_device.cuh
@@ -28,11 +30,22 @@ struct AnnealParams {
   double* final_entropy;
   int32_t* status;
   int64_t* status_step;
-  double* workspace;  // HBM tier: per-CTA psi/psi' slabs
+  double* workspace;  // HBM tier: per-cluster psi/psi' slabs
+  uint64_t slab_clusters;  // HBM tier: slabs the workspace holds (launch_anneal_hbm clamps to it)
   int64_t* trace;     // phase-trace probe only: clock64 stamps [steps][8] of CTA 0's first row
   const GateRec* gates;        // [rows][steps] proposal stream (gate_stream.cu)
   const double* init_states;   // [rows][2^S] interleaved, unnormalised (random start) or null
   int32_t light_fence;         // HBM tier: no GPU-scope fence between gate pass and GEMM (A/B knob)
+  double* status_norm;         // [rows] or null: ||psi|| of a failed norm check
+  int64_t* initial_wall_ns;    // [rows] or null: initial state + entropy, %globaltimer ns
+  unsigned long long* tie_stats;  // [2] or null: fallback decisions, near ties (atomic counters)
+  tg_near_tie* tie_log;        // [tie_capacity] or null
+  uint64_t tie_capacity;
+  double tie_eps;              // near tie: |u - p| < tie_eps (1e-9; TG_NEAR_TIE_EPS widens it in tests)
+  int32_t gate_fault;          // tg_anneal_config inject_fault == 2: the gate of
+  uint64_t fault_procedure;    // (fault_procedure, fault_step) is scaled by 1.001
+  uint64_t fault_step;
+  uint64_t fault_row1;         // 1 + its row in this launch (0 = not in it; zero-init safe), per batch
 };
 
 // Pre-generated proposal stream of one launch (gate_stream.cu).
@@ -53,6 +66,7 @@ cudaError_t launch_gate_stream(const AnnealParams& p, void* ws, size_t ws_bytes,
 enum : int32_t { kRowOk = 0, kRowNotNormalized = 2 };
 
 constexpr int kSmemMaxSpins = 12;
+constexpr uint64_t kMaxSteps = uint64_t{1} << 22;  // gate_stream.cu jump tables (kJumpBits)
 constexpr int kVnMaxSpins = 15;  // device von Neumann: d_a <= 64 (vn.cuh: SMEM tier, HBM tier S=13), d_a = 128 (vn_packed.cuh: S=14,15)
 
 // anneal_smem.cu (S <= 12)
@@ -66,6 +80,7 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
                               bool trace = false);
 cudaError_t launch_finish_renyi(const AnnealParams& p, cudaStream_t stream);
 size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind);
+uint64_t anneal_hbm_slab_clusters(uint64_t rows, int device);  // slabs for launches of <= rows replicas
 
 // probes.cu
 cudaError_t probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* d_out, cudaStream_t s);

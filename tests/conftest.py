@@ -59,3 +59,14 @@ def device():
     dev = tg.Device([0])
     yield dev
     dev.close()
+
+
+def cfg_from_golden(g, procedures=None):
+    """The device ExperimentConfig of a golden trajectory fixture."""
+    import paper_2203_09353_b200 as tg
+    return tg.ExperimentConfig(
+        spins=int(g["spins"]), steps=int(g["steps"]), procedures=procedures or int(g["procedures"]),
+        seed=int(g["seed"]), objective="max" if int(g["objective"]) == 0 else "min",
+        initial_state="product" if int(g["initial_state"]) == 0 else "random",
+        t0=float(g["t0"]), t_min=float(g["t_min"]), renormalize_interval=int(g["renorm"]),
+        entropy_kind="renyi-2" if entropy_kind_of(g) == 1 else "von-neumann")

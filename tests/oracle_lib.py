@@ -210,6 +210,8 @@ class RefLib:
         L.tgr_acceptance.restype = C.c_double
         L.tgr_run_pool.argtypes = [C.POINTER(CConfig), C.c_uint64, C.c_uint64, C.c_int, _dp, _dp, _u8p,
                                    _u8p, C.POINTER(C.c_int64)]
+        L.tgr_time_sample.argtypes = [C.POINTER(CConfig), C.c_uint64, C.c_uint64, C.c_int,
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.tgr_run_experiment.argtypes = [C.POINTER(CConfig), C.c_uint64, C.c_uint64, C.c_char_p, _dp, _dp,
                                          _u8p, _dp, C.POINTER(C.c_int64)]
 
@@ -274,6 +276,19 @@ class RefLib:
         if rc != 0:
             raise RuntimeError(f"reference run failed ({rc}): {self.err()}")
         return Traces(init, ent, acc, st), wall.value
+
+    def time_sample(self, cfg: McCfg, p0: int, count: int, threads: int):
+        """Pooled mc_procedure runs; per replica the total wall ns and the sum of its
+        per-step wall times (ref_driver.cpp tgr_time_sample). Returns (total, steps, wall)."""
+        total = np.zeros(count, np.int64)
+        steps = np.zeros(count, np.int64)
+        wall = C.c_int64()
+        cc = cfg.c()
+        rc = self.L.tgr_time_sample(C.byref(cc), p0, count, threads, _ptr(total, C.POINTER(C.c_int64)),
+                                    _ptr(steps, C.POINTER(C.c_int64)), C.byref(wall))
+        if rc != 0:
+            raise RuntimeError(f"reference sample failed ({rc}): {self.err()}")
+        return total, steps, wall.value
 
     def run_experiment(self, cfg: McCfg, procedures: int, devices: int = 1, mode: str = "cpu-reference"):
         init = np.zeros(procedures)

@@ -6,7 +6,7 @@ import math
 
 import numpy as np
 import pytest
-from conftest import TRAJ_CASES, VN_CASES, entropy_kind_of, load_traj
+from conftest import TRAJ_CASES, VN_CASES, cfg_from_golden, entropy_kind_of, load_traj
 from oracle_lib import McCfg
 
 import paper_2203_09353_b200 as tg
@@ -225,12 +225,7 @@ def test_t6_analytic_entropies():
 
 # ------------------------------------------------------------ T7 trajectories vs reference
 def cfg_from(g, procedures=None):
-    return tg.ExperimentConfig(
-        spins=int(g["spins"]), steps=int(g["steps"]), procedures=procedures or int(g["procedures"]),
-        seed=int(g["seed"]), objective="max" if int(g["objective"]) == 0 else "min",
-        initial_state="product" if int(g["initial_state"]) == 0 else "random",
-        t0=float(g["t0"]), t_min=float(g["t_min"]), renormalize_interval=int(g["renorm"]),
-        entropy_kind="renyi-2" if entropy_kind_of(g) == 1 else "von-neumann")
+    return cfg_from_golden(g, procedures)
 
 
 def assert_traj_parity(rep, g, rows=None):
@@ -368,7 +363,7 @@ def test_t8_hbm_tier_rerun_bitwise(device):
 def test_t9_fault_injection_detected(device):
     g = load_traj("s12")
     cfg = cfg_from(g)
-    cfg.inject_fault = True
+    cfg.inject_fault = 1
     rep = device.run(cfg)
     assert not close(rep.initial_entropy, g["initial"]).all() or not close(rep.entropies, g["entropies"]).all()
 
@@ -470,3 +465,29 @@ def test_largest_chains_invariants(monkeypatch, spins):
     assert 0 <= a.initial_entropy[0] <= bound
     # a Haar-random state of 2^S amplitudes is close to maximally entangled (Page)
     assert a.initial_entropy[0] > bound - 1.5
+
+
+def test_hbm_split_launch_geometry(device, oracle):
+    """with pinned trace arrays tg_anneal_run launches all full waves first
+    (here rows 0..147 of 174 at L = 13: 148 one-CTA clusters) although the workspace was sized
+    for the whole batch's geometry (74 two-CTA clusters). The slab region is now sized for any
+    launch of <= rows replicas (min(rows, SMs) slabs) and the launch clamps to it: pinned
+    (split) and pageable (single launch) runs are bitwise equal and match the oracle."""
+    import torch
+    cfg = tg.ExperimentConfig(spins=13, steps=5, procedures=174, seed=9)
+    rows, steps = 174, 5
+    pinned = {
+        "initial": torch.empty(rows, dtype=torch.float64, pin_memory=True).numpy(),
+        "final": torch.empty(rows, dtype=torch.float64, pin_memory=True).numpy(),
+        "entropies": torch.empty((rows, steps), dtype=torch.float64, pin_memory=True).numpy(),
+        "accepted": torch.empty((rows, steps), dtype=torch.uint8, pin_memory=True).numpy(),
+        "sites": torch.empty((rows, steps), dtype=torch.uint8, pin_memory=True).numpy(),
+    }
+    a = device.run(cfg, out=pinned)
+    b = device.run(cfg)
+    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
+    assert np.array_equal(a.accepted, b.accepted)
+    for p in (0, 73, 147, 148, 173):
+        _, ent, acc, sites, _, _ = oracle.mc_procedure(McCfg(spins=13, steps=steps, seed=9), p)
+        assert np.array_equal(a.accepted[p], acc) and np.array_equal(a.sites[p], sites)
+        assert close(a.entropies[p], ent).all()

@@ -80,3 +80,33 @@ def test_batched_gemm_reference_types(tgi):
     assert "fixed-size" in tgi.tgi_last_error().decode()
     assert tgi.tgi_batched_gemm(2, 0, 4, 4, 4, C.byref(err)) == 2
     assert "non-empty" in tgi.tgi_last_error().decode()
+
+
+@pytest.mark.parametrize("spins,steps,procs,devices,kind", [(8, 50, 7, 1, 1), (14, 6, 5, 1, 1), (10, 20, 4, 1, 0)])
+def test_run_report_complete_through_report_io(tgi, spins, steps, procs, devices, kind):
+    """RunReport from run_experiment_device has what the reference fills (bench.cpp:396-415):
+    per-step wall times, per device its procedures, one KernelRecord per GEMM and metrics;
+    the reference's own report_io serialises it (report_json / kernel_csv / trace_csv)."""
+    import json
+    fn = tgi.tgi_run_experiment_report
+    fn.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_double, C.c_char_p,
+                   C.c_uint64, C.POINTER(C.c_uint64)]
+    buf = C.create_string_buffer(1 << 20)
+    stats = (C.c_uint64 * (devices + 5))()
+    rc = fn(spins, steps, procs, devices, kind, 0, 1e-3, buf, len(buf), stats)
+    assert rc == 0, tgi.tgi_last_error()
+    rep = json.loads(buf.value.decode())
+    assert len(rep["per_device"]) == devices
+    da, db = 1 << (spins // 2), 1 << (spins - spins // 2)
+    for d, dev in enumerate(rep["per_device"]):
+        mine = list(range(d, procs, devices))
+        assert dev["device_id"] == d and dev["procedures"] == mine
+        assert dev["kernel_count"] == len(mine) * (steps + 1) == stats[d]
+        assert dev["total_flops"] == dev["kernel_count"] * 8 * da * da * db
+        assert 1 <= dev["high_water_concurrency"] <= len(mine)
+        assert dev["makespan_ns"] > 0 and dev["busy_ns"] == dev["makespan_ns"] and dev["idle_ns"] == 0
+        assert dev["per_gemm_throughput_median"] > 0 and dev["total_throughput_flops_per_s"] > 0
+    assert stats[devices] == procs * steps  # every per-step wall time > 0
+    assert stats[devices + 1] == 1 + procs * (steps + 1)  # kernel_csv: header + one line per GEMM
+    assert stats[devices + 2] == 1 + procs * steps  # trace_csv
+    assert stats[devices + 4] == 0  # no near ties at the default threshold
