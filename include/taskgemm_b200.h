@@ -193,7 +193,19 @@ tg_status tg_set_perturb_gemm(int on);
  * denominator (no FP64 entry exists in MEASURED_PEAKS.json). */
 tg_status tg_fp64_dmma_peak(int device, double* tflops, double* sm_clock_ghz_est);
 
+/* Which schedule the HBM tier (13 <= spins <= 24) would run a launch of `rows` replicas
+ * with on the current device: 0 = cluster schedule (1, 2 or 4 CTAs own a replica),
+ * 1 = work queue (every CTA pulls tile / gate / decision items), -1 = not an HBM-tier
+ * launch. Diagnostic: replaces nothing in the reference (whose scheduler is the simulated
+ * VirtualDevice, exec.cpp:51-142, out of scope). */
+int tg_hbm_schedule(uint32_t spins, uint64_t rows, int32_t entropy_kind);
+
 /* ---- device-piece probes (parity tests T1-T6 in SURVEY.md §4) ---------------------- */
+/* Work-queue schedule statistics (profiling probe): runs `replicas` x `steps` at `spins`
+ * (13..24) on the queue schedule and writes 16 per-CTA clock64 counters per CTA into
+ * stats[ctas * 16] (layout in csrc/hbm_queue.cuh, STATS); *ctas = the grid size (SM count,
+ * stats must hold 16 * SM count values). */
+tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* stats, int* ctas);
 /* first n xoshiro256++ outputs of derive_stream({seed,p}) computed on the GPU */
 tg_status tg_probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* out_host);
 /* gate stream of `steps` steps (site, U[32], u_accept) generated by the device producer */

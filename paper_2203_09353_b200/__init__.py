@@ -117,7 +117,7 @@ EXPORTS = [
     "tg_fp64_dmma_peak", "tg_probe_rng", "tg_probe_gates", "tg_probe_apply_gate",
     "tg_probe_entropy", "tg_probe_entropy_kind", "tg_probe_phase_trace", "tg_probe_rng_chunking",
     "tg_rng_jump_words", "tg_rng_chunk_steps",
-    "tg_set_perturb_gemm",
+    "tg_set_perturb_gemm", "tg_hbm_schedule", "tg_probe_queue_stats",
 ]
 
 _dp = C.POINTER(C.c_double)
@@ -162,6 +162,8 @@ def lib() -> C.CDLL:
     L.tg_probe_entropy.argtypes = [C.c_uint32, C.c_uint64, _dp, _dp, _dp]
     L.tg_probe_entropy_kind.argtypes = [C.c_uint32, C.c_uint64, _dp, C.c_int32, _dp, _dp]
     L.tg_set_perturb_gemm.argtypes = [C.c_int]
+    L.tg_hbm_schedule.argtypes = [C.c_uint32, C.c_uint64, C.c_int32]
+    L.tg_probe_queue_stats.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]
     L.tg_probe_phase_trace.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64)]
     L.tg_probe_rng_chunking.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int32, C.c_uint64,
                                         C.POINTER(C.c_uint64)]

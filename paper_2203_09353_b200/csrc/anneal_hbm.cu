@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "hbm_queue.cuh"
 #include "hbm_tier.cuh"
 #include "tg_internal.h"
 #include "vn.cuh"
@@ -27,21 +28,6 @@
 namespace tg {
 namespace hbm {
 
-constexpr int kMaxCS = 4;
-struct HHeader {
-  GateRec rec[2];                    // proposal records of steps s, s + 1 (prefetched)
-  double part[kWarps][2 * kChains];  // per-warp chain values {rho chain 0..3, tr chain 0..3}
-  double val[kMaxCS][2 * kChains];   // per-rank chain sums (other ranks' arrive by DSMEM)
-  double norm_q[4];                  // renormalisation: sums over the four quarters of psi
-  uint64_t full[kStages];            // TMA pipeline (rho_partials_tma)
-  uint64_t empty[kStages];
-  int32_t decision;
-  int32_t error;
-};
-constexpr int kHHeaderBytes = (static_cast<int>(sizeof(HHeader)) + 127) / 128 * 128;
-// + 1 KB: the anneal kernel aligns its stages to 1 KB (the TMA swizzle is a function of the
-// SMEM address bits)
-constexpr int kSmemBytes = kHHeaderBytes + kStages * kStage * 8 + 1024;
 // von Neumann (KIND 1, S = 13: d_a = 64 = one tile, CS = 1): rho planes (pitch 68) and the
 // solver scratch reuse the stage buffers once the GEMM pipeline has drained.
 constexpr int kRP = TB + 4;
@@ -51,76 +37,6 @@ static_assert(2 * TB * kRP * 8 + static_cast<int>(sizeof(vn::Scratch)) <= kStage
 constexpr int kPackedN = vnp::kMaxN;
 constexpr int kPackedPlane = (vnp::packed_size(kPackedN) + 15) / 16 * 16;
 static_assert(2 * kPackedPlane * 8 + static_cast<int>(sizeof(vnp::Scratch)) <= kStages * kStage * 8, "vN packed region");
-
-template <int CS>
-__device__ __forceinline__ void sync_all() {
-  if constexpr (CS == 1) {
-    __syncthreads();
-  } else {
-    cluster_sync();
-  }
-}
-
-// Per-rank values (sum of the per-warp chain values in warp order) published to every rank.
-template <int CS>
-__device__ __forceinline__ void publish_vals(HHeader& H, int tid, uint32_t rank) {
-  __syncthreads();  // per-warp parts written
-  if (tid < 2 * kChains) {
-    double v = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) v += H.part[w][tid];
-    H.val[rank][tid] = v;
-#pragma unroll
-    for (uint32_t d = 1; d < static_cast<uint32_t>(CS); ++d) st_cluster_f64(&H.val[rank][tid], (rank + d) % CS, v);
-  }
-  sync_all<CS>();
-}
-
-// Totals in the canonical order ((c0 + c1) + (c2 + c3)); chain c was summed by rank c % CS.
-template <int CS>
-__device__ __forceinline__ void totals(const HHeader& H, double& rho2, double& tr) {
-  auto v = [&](int k) { return H.val[(k % kChains) % CS][k]; };
-  rho2 = (v(0) + v(1)) + (v(2) + v(3));
-  tr = (v(4) + v(5)) + (v(6) + v(7));
-}
-
-// renormalize (spinmc.cpp:56-59) over the four quarters of psi (rank k owns quarters
-// q = k mod CS); the total is ((q0 + q1) + (q2 + q3)) whatever CS is, so every CS agrees
-// bitwise.
-template <int CS>
-__device__ void renormalize(const Geo& G, double* X, double* Y, int tid, int warp, int lane,
-                            uint32_t rank, HHeader& H) {
-  const int quarter = G.n / 4;
-  for (int q = static_cast<int>(rank); q < 4; q += CS) {
-    double s = 0.0;
-    for (int i = q * quarter + tid; i < (q + 1) * quarter; i += kThreads) {
-      const double x = __ldcg(X + i), y = __ldcg(Y + i);
-      s = fma(x, x, s);
-      s = fma(y, y, s);
-    }
-    s = warp_sum(s);
-    if (lane == 0) H.part[warp][0] = s;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) t += H.part[w][0];
-      H.norm_q[q] = t;
-      for (uint32_t d = 1; d < static_cast<uint32_t>(CS); ++d) st_cluster_f64(&H.norm_q[q], (rank + d) % CS, t);
-    }
-    __syncthreads();
-  }
-  sync_all<CS>();
-  const double inv = __ddiv_rn(1.0, __dsqrt_rn((H.norm_q[0] + H.norm_q[1]) + (H.norm_q[2] + H.norm_q[3])));
-  const int part = G.n / CS, i0 = static_cast<int>(rank) * part, i1 = i0 + part;
-  for (int i = i0 + tid; i < i1; i += kThreads) {
-    __stcg(X + i, __dmul_rn(__ldcg(X + i), inv));
-    __stcg(Y + i, __dmul_rn(__ldcg(Y + i), inv));
-  }
-  __threadfence();
-  fence_proxy_async_global();  // the next GEMM may read psi through the TMA engine
-  sync_all<CS>();
-}
 
 // TRACE: phase stamps (clock64) of the first cluster's first replica into P.trace[steps][8]:
 // 0 step start, 1 gate pass done, 2 GEMM done, 3 decision done (profiling probe only).
@@ -584,21 +500,107 @@ uint64_t anneal_hbm_slab_clusters(uint64_t rows, int device) {
   return std::min<uint64_t>(rows, static_cast<uint64_t>(sms > 0 ? sms : 1));
 }
 
+namespace {
+
+// Work-queue schedule (hbm_queue.cuh): Renyi-2 with TMA staging, every row's slab resident at
+// once, so the row count is bounded by memory (and the queue only pays where the cluster
+// schedule leaves SMs idle, i.e. small and medium batches).
+constexpr size_t kQueueSlabBudget = size_t{48} << 30;
+constexpr uint64_t kQueueMaxRows = 8192;
+
+bool queue_possible(uint32_t spins, uint64_t rows, int entropy_kind) {
+  if (entropy_kind != TG_RENYI2 || rows == 0 || rows > kQueueMaxRows || !hbm_use_tma()) return false;
+  const char* env = std::getenv("TG_HBM_QUEUE");
+  if (env && env[0] == '0') return false;
+  return rows * (size_t{32} << spins) <= kQueueSlabBudget;
+}
+
+// Schedule choice by a tile-time model. Cluster schedule: ceil(rows / clusters) waves of
+// ceil(ntt / cs) tiles per CTA; queue: ceil(rows * ntt / sms) tiles per CTA. Each is scaled
+// by its measured per-tile overhead at this chain length (gate pass, decision, pipeline
+// refills; queue: also the per-item handoffs, which weigh more the fewer tiles a replica
+// has): profiles/r02_queue_vs_cluster.txt.
+// TG_HBM_QUEUE=1 forces the queue, =0 the cluster schedule; TG_HBM_CTAS_PER_REPLICA or the
+// phase-trace probe force the cluster schedule.
+bool queue_pick(uint32_t spins, uint64_t rows, int entropy_kind, int device, bool trace) {
+  if (trace || !queue_possible(spins, rows, entropy_kind)) return false;
+  const char* env = std::getenv("TG_HBM_QUEUE");
+  if (env && env[0] == '1') return true;
+  if (std::getenv("TG_HBM_CTAS_PER_REPLICA")) return false;
+  int sms = 0, cs = 1;
+  uint64_t clusters = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (hbm_geometry(spins, rows, entropy_kind, device, cs, clusters) != cudaSuccess || clusters == 0 || sms <= 0)
+    return false;
+  const uint64_t nt = (uint64_t{1} << (spins / 2)) / hbm::TB, ntt = nt * nt;
+  static const double kQueueOver[] = {0.8, 0.6, 0.35, 0.2, 0.1};     // S = 13..17, then 0.05
+  static const double kClusterOver[] = {0.25, 0.2, 0.12, 0.1, 0.08};  // S = 13..17, then 0.07
+  const double qo = spins <= 17 ? kQueueOver[spins - 13] : 0.05;
+  const double co = spins <= 17 ? kClusterOver[spins - 13] : 0.07;
+  const double t_cluster = static_cast<double>((rows + clusters - 1) / clusters) *
+                           static_cast<double>((ntt + cs - 1) / cs) * (1.0 + co);
+  const double t_queue = static_cast<double>((rows * ntt + sms - 1) / sms) * (1.0 + qo);
+  return t_queue < t_cluster;
+}
+
+}  // namespace
+
+uint64_t anneal_hbm_queue_rows(uint32_t spins, uint64_t rows, int entropy_kind) {
+  return queue_possible(spins, rows, entropy_kind) ? rows : 0;
+}
+
+int anneal_hbm_schedule(const AnnealParams& p, int device) {
+  return queue_pick(p.spins, p.rows, p.entropy_kind, device, false) ? 1 : 0;
+}
+
+// [max(cluster slabs, queue rows) slabs][queue region (partials, row state, counters)]
 size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind) {
   const uint64_t clusters = anneal_hbm_slab_clusters(rows, device);
+  const uint64_t qrows = anneal_hbm_queue_rows(spins, rows, entropy_kind);
   const size_t da = size_t{1} << (spins / 2);
   // von Neumann with d_a > 64: rho (2 planes of d_a^2) after each slab (vn_packed.cuh)
   const size_t rho = entropy_kind == 0 && da > static_cast<size_t>(hbm::TB) ? 2 * da * da : 0;
-  return static_cast<size_t>(clusters) * (4 * (size_t{1} << spins) + rho) * sizeof(double);
+  const size_t slab = (4 * (size_t{1} << spins) + rho) * sizeof(double);
+  return static_cast<size_t>(std::max(clusters, qrows)) * slab + (qrows ? hbmq::QLayout::bytes(spins, qrows) : 0);
 }
 
 uint64_t anneal_hbm_wave_rows(const AnnealParams& p) {  // co-resident clusters = replicas per wave
   int dev = 0, cs = 1;
   uint64_t clusters = 0;
   cudaGetDevice(&dev);
+  if (queue_pick(p.spins, p.rows, p.entropy_kind, dev, false)) return p.rows;  // one wave: every row at once
   if (hbm_geometry(p.spins, p.rows, p.entropy_kind, dev, cs, clusters) != cudaSuccess) return 0;
   return clusters;
 }
+
+namespace {
+
+cudaError_t launch_queue(const AnnealParams& p, cudaStream_t stream, int dev, int* grid_out, bool stats) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  cudaError_t e = hbm_tensor_map(p, p.rows, &tmap);  // slot = row
+  if (e != cudaSuccess) return e;
+  const hbmq::QLayout L(reinterpret_cast<char*>(p.workspace + p.queue_rows * 4 * (uint64_t{1} << p.spins)), p.spins,
+                        p.queue_rows);
+  e = cudaMemsetAsync(L.ctr, 0, L.counter_bytes, stream);
+  if (e != cudaSuccess) return e;
+  auto kern = stats ? hbmq::anneal_queue_kernel<true> : hbmq::anneal_queue_kernel<false>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbmq::kQSmemBytes);
+  if (e != cudaSuccess) return e;
+  const int grid = sms > 0 ? sms : 1;  // one CTA per SM; the queue is deadlock-free at any residency
+  if (grid_out) *grid_out = grid;
+  if (std::getenv("TG_VERBOSE"))
+    std::fprintf(stderr, "[tg] hbm work queue: spins %u rows %llu on %d CTAs\n", p.spins,
+                 static_cast<unsigned long long>(p.rows), grid);
+  kern<<<grid, hbmq::kQThreads, hbmq::kQSmemBytes, stream>>>(p, tmap);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_finish_renyi(p, stream);
+}
+
+}  // namespace
 
 cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* grid_out,
                               bool trace) {
@@ -608,6 +610,13 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   int dev = 0, cs = 1;
   uint64_t clusters = 0;
   cudaGetDevice(&dev);
+  // the phase-trace probe runs the cluster schedule; with TG_HBM_QUEUE=1 it runs the queue's
+  // per-CTA statistics instead (tg_probe_queue_stats)
+  const char* qenv = std::getenv("TG_HBM_QUEUE");
+  const bool queue_stats = trace && qenv && qenv[0] == '1';
+  if (p.rows > 0 && p.queue_rows >= p.rows &&
+      (queue_stats ? queue_possible(p.spins, p.rows, p.entropy_kind) : queue_pick(p.spins, p.rows, p.entropy_kind, dev, trace)))
+    return launch_queue(p, stream, dev, grid_out, queue_stats);
   cudaError_t e = hbm_geometry(p.spins, p.rows, p.entropy_kind, dev, cs, clusters);
   if (e != cudaSuccess) return e;
   // never more clusters than the workspace has slabs (the persistent loop strides over rows)

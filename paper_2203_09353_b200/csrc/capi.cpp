@@ -198,6 +198,7 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
     q.init_states = gs.init_states;
     q.workspace = reinterpret_cast<double*>(slabs);
     q.slab_clusters = slab_clusters(p.spins, batch, dev);
+    q.queue_rows = p.spins > static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::anneal_hbm_queue_rows(p.spins, batch, p.entropy_kind) : 0;
     e = p.spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) ? tg::launch_anneal_smem(q, s, nullptr, trace)
                                                            : tg::launch_anneal_hbm(q, s, nullptr, trace);
     if (e != cudaSuccess) return e;
@@ -661,6 +662,20 @@ tg_status tg_fp64_dmma_peak(int device, double* tflops, double* clock_ghz) {
   return TG_OK;
 }
 
+int tg_hbm_schedule(uint32_t spins, uint64_t rows, int32_t entropy_kind) {
+  if (spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) || spins > 24) return -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  tg::AnnealParams p{};
+  p.spins = spins;
+  p.rows = rows;
+  p.entropy_kind = entropy_kind;
+  return tg::anneal_hbm_schedule(p, dev);
+}
+
 // ------------------------------------------------------------------------- probes
 tg_status tg_probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* out) {
   uint64_t* d = nullptr;
@@ -790,6 +805,49 @@ tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps
   cudaFree(ws);
   cudaFree(d);
   if (e != cudaSuccess) return cuda_fail(e, "probe_phase_trace");
+  return TG_OK;
+}
+
+tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* stats, int* ctas) {
+  if (spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) || spins > 24) return fail(TG_EINVAL, "queue stats cover spins in [13,24]");
+  if (!stats || !ctas) return fail(TG_EINVAL, "stats / ctas must not be NULL");
+  setenv("TG_HBM_QUEUE", "1", 1);
+  tg_anneal_config c{};
+  c.spins = spins;
+  c.devices = 1;
+  c.steps = steps;
+  c.procedures = replicas;
+  c.entropy_kind = TG_RENYI2;
+  c.t0 = 1.0;
+  c.t_min = 1e-3;
+  c.renormalize_interval = 1000;
+  c.shard_count = 1;
+  tg::AnnealParams p = make_params(&c, replicas, 0, 1);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  char* d = nullptr;
+  const size_t bytes = trace_bytes(replicas, steps, false, false) + 128 * static_cast<size_t>(sms) + 256;
+  TG_CUDA(cudaMalloc(&d, bytes));
+  char* cur = d;
+  p.initial_entropy = carve<double>(cur, replicas);
+  p.final_entropy = carve<double>(cur, replicas);
+  p.status = carve<int32_t>(cur, replicas);
+  p.status_step = carve<int64_t>(cur, replicas);
+  p.entropies = carve<double>(cur, replicas * steps);
+  p.accepted = carve<uint8_t>(cur, replicas * steps);
+  p.trace = carve<int64_t>(cur, 16 * static_cast<size_t>(sms));
+  const size_t wsb = workspace_for(p, dev);
+  void* ws = nullptr;
+  cudaError_t e = cudaMalloc(&ws, wsb);
+  if (e == cudaSuccess) e = cudaMemset(p.trace, 0, 128 * static_cast<size_t>(sms));
+  if (e == cudaSuccess) e = launch(p, ws, wsb, nullptr, /*trace=*/true);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(stats, p.trace, 128 * static_cast<size_t>(sms), cudaMemcpyDeviceToHost);
+  cudaFree(ws);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "probe_queue_stats");
+  *ctas = sms;
   return TG_OK;
 }
 

@@ -171,6 +171,10 @@ __device__ __forceinline__ void load_stage(const double* X, const double* Y, int
   }
 }
 
+// inject_fault: flip the sign of the first accumulation term of rho(0,0) (linalg.cpp:94).
+// One definition for every schedule (cluster and queue), so their rounding is the same.
+__device__ __forceinline__ void fault_term(double& c, double x0, double y0) { c -= 2.0 * (x0 * x0 + y0 * y0); }
+
 // Tile epilogue, part 1: the diagonal tile's trace into chain ch; the fault injection.
 __device__ __forceinline__ void tile_trace_fault(double (&cr)[2][4][2], double (&tr)[kChains], int ch, bool diag,
                                                  bool fault, const double* X, const double* Y, int wr, int wc,
@@ -190,7 +194,7 @@ __device__ __forceinline__ void tile_trace_fault(double (&cr)[2][4][2], double (
 #pragma unroll
     for (int c = 0; c < kChains; ++c) tr[c] = c == ch ? tsum : tr[c];
   }
-  if (fault && wr == 0 && wc == 0 && lane == 0) cr[0][0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);
+  if (fault && wr == 0 && wc == 0 && lane == 0) fault_term(cr[0][0][0], X[0], Y[0]);
 }
 
 // Tile epilogue, part 2: the tile's sum |rho_ij|^2 into chain ch, in four interleaved
@@ -514,6 +518,93 @@ __device__ __forceinline__ void rho_partials_tma(const Geo& G, const void* tmap,
     out[c] = warp_sum(rho[c]);
     out[kChains + c] = warp_sum(tr[c]);
   }
+}
+
+// ------------------------------------------------- per-CTA header, shared helpers
+constexpr int kMaxCS = 4;
+struct HHeader {
+  GateRec rec[2];                    // proposal records of steps s, s + 1 (prefetched)
+  double part[kWarps][2 * kChains];  // per-warp chain values {rho chain 0..3, tr chain 0..3}
+  double val[kMaxCS][2 * kChains];   // per-rank chain sums (other ranks' arrive by DSMEM)
+  double norm_q[4];                  // renormalisation: sums over the four quarters of psi
+  uint64_t full[kStages];            // TMA pipeline (rho_partials_tma)
+  uint64_t empty[kStages];
+  int32_t decision;
+  int32_t error;
+};
+constexpr int kHHeaderBytes = (static_cast<int>(sizeof(HHeader)) + 127) / 128 * 128;
+// + 1 KB: the anneal kernel aligns its stages to 1 KB (the TMA swizzle is a function of the
+// SMEM address bits)
+constexpr int kSmemBytes = kHHeaderBytes + kStages * kStage * 8 + 1024;
+
+template <int CS>
+__device__ __forceinline__ void sync_all() {
+  if constexpr (CS == 1) {
+    __syncthreads();
+  } else {
+    cluster_sync();
+  }
+}
+
+// Per-rank values (sum of the per-warp chain values in warp order) published to every rank.
+template <int CS>
+__device__ __forceinline__ void publish_vals(HHeader& H, int tid, uint32_t rank) {
+  __syncthreads();  // per-warp parts written
+  if (tid < 2 * kChains) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) v += H.part[w][tid];
+    H.val[rank][tid] = v;
+#pragma unroll
+    for (uint32_t d = 1; d < static_cast<uint32_t>(CS); ++d) st_cluster_f64(&H.val[rank][tid], (rank + d) % CS, v);
+  }
+  sync_all<CS>();
+}
+
+// Totals in the canonical order ((c0 + c1) + (c2 + c3)); chain c was summed by rank c % CS.
+template <int CS>
+__device__ __forceinline__ void totals(const HHeader& H, double& rho2, double& tr) {
+  auto v = [&](int k) { return H.val[(k % kChains) % CS][k]; };
+  rho2 = (v(0) + v(1)) + (v(2) + v(3));
+  tr = (v(4) + v(5)) + (v(6) + v(7));
+}
+
+// renormalize (spinmc.cpp:56-59) over the four quarters of psi (rank k owns quarters
+// q = k mod CS); the total is ((q0 + q1) + (q2 + q3)) whatever CS is, so every CS agrees
+// bitwise.
+template <int CS>
+__device__ void renormalize(const Geo& G, double* X, double* Y, int tid, int warp, int lane,
+                            uint32_t rank, HHeader& H) {
+  const int quarter = G.n / 4;
+  for (int q = static_cast<int>(rank); q < 4; q += CS) {
+    double s = 0.0;
+    for (int i = q * quarter + tid; i < (q + 1) * quarter; i += kThreads) {
+      const double x = __ldcg(X + i), y = __ldcg(Y + i);
+      s = fma(x, x, s);
+      s = fma(y, y, s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) H.part[warp][0] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) t += H.part[w][0];
+      H.norm_q[q] = t;
+      for (uint32_t d = 1; d < static_cast<uint32_t>(CS); ++d) st_cluster_f64(&H.norm_q[q], (rank + d) % CS, t);
+    }
+    __syncthreads();
+  }
+  sync_all<CS>();
+  const double inv = __ddiv_rn(1.0, __dsqrt_rn((H.norm_q[0] + H.norm_q[1]) + (H.norm_q[2] + H.norm_q[3])));
+  const int part = G.n / CS, i0 = static_cast<int>(rank) * part, i1 = i0 + part;
+  for (int i = i0 + tid; i < i1; i += kThreads) {
+    __stcg(X + i, __dmul_rn(__ldcg(X + i), inv));
+    __stcg(Y + i, __dmul_rn(__ldcg(Y + i), inv));
+  }
+  __threadfence();
+  fence_proxy_async_global();  // the next GEMM may read psi through the TMA engine
+  sync_all<CS>();
 }
 
 cudaError_t probe_apply_gate(uint32_t spins, const double* psi, int site, const double* u,

@@ -32,6 +32,7 @@ struct AnnealParams {
   int64_t* status_step;
   double* workspace;  // HBM tier: per-cluster psi/psi' slabs
   uint64_t slab_clusters;  // HBM tier: slabs the workspace holds (launch_anneal_hbm clamps to it)
+  uint64_t queue_rows;     // HBM tier: rows the workspace's work-queue region is sized for (0 = none)
   int64_t* trace;     // phase-trace probe only: clock64 stamps [steps][8] of CTA 0's first row
   const GateRec* gates;        // [rows][steps] proposal stream (gate_stream.cu)
   const double* init_states;   // [rows][2^S] interleaved, unnormalised (random start) or null
@@ -80,7 +81,10 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
                               bool trace = false);
 cudaError_t launch_finish_renyi(const AnnealParams& p, cudaStream_t stream);
 size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int entropy_kind);
+// which HBM-tier schedule a launch of p uses: 0 cluster, 1 work queue (hbm_queue.cuh)
+int anneal_hbm_schedule(const AnnealParams& p, int device);
 uint64_t anneal_hbm_slab_clusters(uint64_t rows, int device);  // slabs for launches of <= rows replicas
+uint64_t anneal_hbm_queue_rows(uint32_t spins, uint64_t rows, int entropy_kind);  // queue region capacity
 
 // probes.cu
 cudaError_t probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* d_out, cudaStream_t s);

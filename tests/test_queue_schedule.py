@@ -1,0 +1,138 @@
+"""GPU: the HBM tier's work-queue schedule (csrc/hbm_queue.cuh) — every CTA pulls INIT / TILE /
+DEC / GATE items from one queue instead of owning whole replicas. Its traces must be bitwise
+those of the cluster schedule (the tiles' per-thread partials are folded in the canonical
+order whichever CTA computed them) and match the oracle (sites and accept flags bit-exact,
+entropies within 1e-10)."""
+import numpy as np
+import pytest
+from oracle_lib import McCfg
+
+import paper_2203_09353_b200 as tg
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def close(got, want, tol=TOL):
+    got, want = np.asarray(got), np.asarray(want)
+    return np.abs(got - want) <= tol * np.maximum(np.abs(want), 1.0)
+
+
+def run_with(device, cfg, monkeypatch, **env):
+    for k in ("TG_HBM_QUEUE", "TG_HBM_CTAS_PER_REPLICA"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    return device.run(cfg, wall=True)
+
+
+def assert_bitwise(a, b):
+    assert np.array_equal(a.initial_entropy.view(np.uint64), b.initial_entropy.view(np.uint64))
+    assert np.array_equal(a.entropies.view(np.uint64), b.entropies.view(np.uint64))
+    assert np.array_equal(a.final_entropy.view(np.uint64), b.final_entropy.view(np.uint64))
+    assert np.array_equal(a.accepted, b.accepted)
+    assert np.array_equal(a.sites, b.sites)
+    assert a.average_entropy == b.average_entropy
+
+
+CASES = [  # spins, procedures, steps, initial state, objective, renormalize_interval
+    (13, 4, 12, "random", "max", 1000),   # d_a = 64: one tile per replica
+    (14, 5, 20, "product", "max", 7),     # renormalisation inside DEC items
+    (14, 1, 30, "random", "min", 9),      # one replica: lag 0, strictly sequential queue
+    (15, 2, 10, "product", "min", 4),
+    (16, 3, 6, "random", "max", 1000),    # 16 tiles, 4 gate parts per replica
+    (14, 37, 8, "product", "max", 1000),  # more replicas than tiles in flight
+    (18, 2, 3, "random", "max", 2),       # 16 gate parts, 64 tiles
+]
+
+
+@pytest.mark.parametrize("spins,procs,steps,init,obj,renorm", CASES)
+def test_queue_vs_cluster_bitwise(device, oracle, monkeypatch, spins, procs, steps, init, obj, renorm):
+    cfg = tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=31, initial_state=init,
+                              objective=obj, renormalize_interval=renorm)
+    a = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="0", TG_HBM_CTAS_PER_REPLICA="1")
+    b = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="1")
+    assert_bitwise(a, b)
+    assert np.all(b.wall_ns > 0)
+    if spins <= 16:
+        want = oracle.run(McCfg(spins=spins, steps=steps, seed=31, initial_state=1 if init == "random" else 0,
+                                objective=1 if obj == "min" else 0, renormalize_interval=renorm), 0, procs)
+        assert np.array_equal(b.sites, want.sites)
+        assert np.array_equal(b.accepted, want.accepted)
+        assert close(b.entropies, want.entropies).all()
+        assert close(b.initial_entropy, want.initial).all()
+
+
+def test_queue_rerun_bitwise_and_zero_steps(device, monkeypatch):
+    cfg = tg.ExperimentConfig(spins=14, steps=15, procedures=9, seed=2)
+    a = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="1")
+    b = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="1")
+    assert_bitwise(a, b)
+    z = tg.ExperimentConfig(spins=14, steps=0, procedures=3, seed=2)
+    c = run_with(device, z, monkeypatch, TG_HBM_QUEUE="1")
+    d = run_with(device, z, monkeypatch, TG_HBM_QUEUE="0", TG_HBM_CTAS_PER_REPLICA="1")
+    assert c.entropies.shape == (3, 0)
+    assert np.array_equal(c.initial_entropy.view(np.uint64), d.initial_entropy.view(np.uint64))
+    assert c.average_entropy == d.average_entropy
+
+
+def test_queue_fault_injection_bitwise(device, monkeypatch):
+    """inject_fault = 1 (perturb_gemm on tile 0 of every GEMM): the queue applies the same
+    perturbation with the same rounding as the cluster schedule."""
+    cfg = tg.ExperimentConfig(spins=14, steps=6, procedures=3, seed=5, inject_fault=1)
+    a = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="0", TG_HBM_CTAS_PER_REPLICA="2")
+    b = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="1")
+    assert_bitwise(a, b)
+
+
+def test_queue_not_normalized_error(device, monkeypatch):
+    """A non-unitary gate (inject_fault = 2) on one replica: the queue schedule reports the
+    reference's std::invalid_argument message, like the cluster schedule."""
+    cfg = tg.ExperimentConfig(spins=14, steps=8, procedures=4, seed=5, inject_fault=2, fault_procedure=2,
+                              fault_step=3)
+    msgs = []
+    for env in ({"TG_HBM_QUEUE": "0", "TG_HBM_CTAS_PER_REPLICA": "1"}, {"TG_HBM_QUEUE": "1"}):
+        with pytest.raises(ValueError, match="entanglement_entropy: state not normalized") as ei:
+            run_with(device, cfg, monkeypatch, **env)
+        msgs.append(str(ei.value))
+    assert msgs[0] == msgs[1]
+
+
+def test_queue_two_contexts_share_gpu(oracle, monkeypatch):
+    """Two host threads (devices [0, 0]) each launch a queue kernel on GPU 0 at the same time:
+    neither grid is fully resident, which the dependency-ordered queue tolerates (no grid
+    barrier); traces are bitwise the one-device run's."""
+    monkeypatch.setenv("TG_HBM_QUEUE", "1")
+    cfg1 = tg.ExperimentConfig(spins=14, steps=12, procedures=6, seed=21, devices=1)
+    cfg2 = tg.ExperimentConfig(spins=14, steps=12, procedures=6, seed=21, devices=2)
+    with tg.Device([0]) as d1:
+        a = d1.run(cfg1)
+    with tg.Device([0, 0]) as d2:
+        b = d2.run(cfg2)
+    assert_bitwise(a, b)
+    want = oracle.run(McCfg(spins=14, steps=12, seed=21), 0, 6)
+    assert np.array_equal(b.accepted, want.accepted)
+
+
+@pytest.mark.slow
+def test_queue_config4_shape(device, oracle, monkeypatch):
+    """L = 20 (256 tiles of 64x64 per replica, 16 gate parts): queue vs 1-CTA cluster
+    bitwise on 3 replicas x 2 steps; replica 0 against the oracle."""
+    cfg = tg.ExperimentConfig(spins=20, steps=2, procedures=3, seed=4)
+    a = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="0", TG_HBM_CTAS_PER_REPLICA="1")
+    b = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="1")
+    assert_bitwise(a, b)
+    _, ent, acc, sites, _, _ = oracle.mc_procedure(McCfg(spins=20, steps=2, seed=4), 0)
+    assert np.array_equal(b.accepted[0], acc) and np.array_equal(b.sites[0], sites)
+    assert close(b.entropies[0], ent).all()
+
+
+def test_queue_schedule_choice():
+    """The model picks the queue where the cluster schedule idles SMs (64 replicas of L = 20:
+    128 of 148 SMs) and keeps the cluster schedule for large batches."""
+    L = tg.lib()
+    if not hasattr(L, "tg_hbm_schedule"):
+        pytest.skip("no schedule probe")
+    assert L.tg_hbm_schedule(20, 64, 1) == 1
+    assert L.tg_hbm_schedule(14, 65536, 1) == 0
+    assert L.tg_hbm_schedule(14, 64, 0) == 0  # von Neumann: cluster schedule only
