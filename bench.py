@@ -237,13 +237,23 @@ def run_reference_arm(args, rank, world):
     return 0
 
 
-def load_traffic(spins, rows, mc_steps):
-    """DRAM bytes per anneal-kernel launch of this exact workload from a committed ncu capture
-    (profiles/ncu_traffic.json), or None when no capture of it exists."""
+def anneal_kernel(L, spins, rows, entropy):
+    """The anneal kernel a launch of this workload runs (csrc: SMEM tier, HBM-tier cluster
+    schedule or HBM-tier work queue, tg_hbm_schedule)."""
+    if spins <= 12:
+        return "anneal_smem_kernel", ""
+    if int(L.tg_hbm_schedule(spins, rows, 0 if entropy == "von-neumann" else 1)) == 1:
+        return "anneal_queue_kernel", "q"
+    return "anneal_hbm_kernel", ""
+
+
+def load_traffic(spins, rows, mc_steps, tag=""):
+    """DRAM bytes per anneal-kernel launch of this exact workload (and schedule) from a
+    committed ncu capture (profiles/ncu_traffic.json), or None when no capture of it exists."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            ent = json.load(f).get(f"{spins}x{rows}x{mc_steps}")
+            ent = json.load(f).get(f"{spins}x{rows}x{mc_steps}{tag}")
         return None if ent is None else float(ent["bytes"])
     except (OSError, ValueError, KeyError, TypeError):
         return None
@@ -323,6 +333,7 @@ def run_ours(args, rank, world, local_rank):
             raise RuntimeError(L.tg_last_error().decode())
 
     peak_tflops, peak_clock = tg.fp64_dmma_peak(gpu)
+    kname, ktag = anneal_kernel(L, spins, rows, args.entropy)
 
     for _ in range(args.warmup):
         launch()
@@ -394,14 +405,14 @@ def run_ours(args, rank, world, local_rank):
             "config": config,
             "tflops": replica_steps * step_flops(spins) / t_step / 1e12,
             "average_entropy": avg, "best_procedure": best, "best_entropy": best_e,
-            "roofline": {"bound": "tensor", "kernel": "anneal_smem_kernel" if spins <= 12 else "anneal_hbm_kernel",
+            "roofline": {"bound": "tensor", "kernel": kname,
                          "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                          "frac": achieved / peak_tflops,
                          "peak_source": f"builder-measured DMMA.8x8x4 peak, live probe (tg_fp64_dmma_peak, "
                                         f"{peak_clock:.3f} GHz); MEASURED_PEAKS.json has no FP64 entry; see "
                                         "profiles/r01_fp64_peak.json",
                          "timed": "tg_anneal_launch on its stream (proposal pre-pass + anneal kernel), CUDA events",
-                         "flops_per_launch": flops_launch, "traffic": load_traffic(spins, rows, S)},
+                         "flops_per_launch": flops_launch, "traffic": load_traffic(spins, rows, S, ktag)},
             "e2e": {"value": replica_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": C.sizeof(ccfg),
                     "d2h_bytes_per_step": d2h * world, "ms_per_step": t_e2e * 1e3},
             "gpu_launches": launches * world,

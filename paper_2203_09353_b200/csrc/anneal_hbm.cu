@@ -533,10 +533,11 @@ bool queue_pick(uint32_t spins, uint64_t rows, int entropy_kind, int device, boo
   if (hbm_geometry(spins, rows, entropy_kind, device, cs, clusters) != cudaSuccess || clusters == 0 || sms <= 0)
     return false;
   const uint64_t nt = (uint64_t{1} << (spins / 2)) / hbm::TB, ntt = nt * nt;
-  static const double kQueueOver[] = {0.8, 0.6, 0.35, 0.2, 0.1};     // S = 13..17, then 0.05
-  static const double kClusterOver[] = {0.25, 0.2, 0.12, 0.1, 0.08};  // S = 13..17, then 0.07
+  // measured (r02_queue_vs_cluster.txt): S = 14: 0.36 / 0.23, 16: 0.175 / 0.15, 20: 0.05 / 0.067
+  static const double kQueueOver[] = {0.5, 0.36, 0.25, 0.175, 0.12};     // S = 13..17, then 0.05
+  static const double kClusterOver[] = {0.3, 0.23, 0.19, 0.15, 0.11};    // S = 13..17, then 0.067
   const double qo = spins <= 17 ? kQueueOver[spins - 13] : 0.05;
-  const double co = spins <= 17 ? kClusterOver[spins - 13] : 0.07;
+  const double co = spins <= 17 ? kClusterOver[spins - 13] : 0.067;
   const double t_cluster = static_cast<double>((rows + clusters - 1) / clusters) *
                            static_cast<double>((ntt + cs - 1) / cs) * (1.0 + co);
   const double t_queue = static_cast<double>((rows * ntt + sms - 1) / sms) * (1.0 + qo);

@@ -19,10 +19,12 @@
 //
 // Queue layout: a prologue of R x (P [+1]) INIT [NORM] items, then blocks k = 0 .. K+lagG-1
 // (K = (steps + 1) R, position k = replica k mod R at step k / R - 1), each
-//   [ntt TILE items of position k] [DEC of position k - lagD] [P GATE items: next step of position k - lagG]
+//   [ntt TILE items of position k] [DEC of position k - lagD] [GATE parts 1..P-1: next step of position k - lagG]
+// (the DEC item applies part 0 of its replica's next gate itself, right after deciding)
 // (slots without work are skipped). lagG < R keeps GATE(r, s+1) ahead of TILE(r, s+1);
 // lagD ~ 2 x grid / ntt tile items lets position k's tiles finish before its DEC is pulled,
-// and lagG = lagD + 1 lets the DEC finish before its gate parts are pulled.
+// and lagG ~ lagD + one CTA round of items lets the DEC finish before its other gate parts
+// are pulled.
 //
 // Determinism. A tile stores its per-thread partials (the ||rho||^2 term tile_fold forms and
 // the diagonal trace terms tile_trace_fault adds) instead of adding them to per-thread
@@ -91,11 +93,12 @@ struct QGeo {
     Ip = P + (random ? 1 : 0);
     rows = r;
     steps = st;
+    BS = ntt + P;  // tiles, DEC (+ gate part 0 of the next step), gate parts 1 .. P-1
     const uint64_t want = (2ull * grid + ntt - 1) / ntt;
     const uint64_t lmax = r > 0 ? r - 1 : 0;
-    lagG = static_cast<uint32_t>(want + 1 < lmax ? want + 1 : lmax);
+    const uint64_t wantG = want + (P > 1 ? (grid + BS - 1) / BS : 0);  // ~ one CTA round after the DEC
+    lagG = static_cast<uint32_t>(wantG < lmax ? wantG : lmax);
     lagD = static_cast<uint32_t>(want < lagG ? want : lagG);
-    BS = ntt + 1 + P;
     pro = r * Ip;
     K = (st + 1) * r;
     total = pro + (K + lagG) * BS;
@@ -136,7 +139,7 @@ struct QGeo {
     if (static_cast<uint64_t>(x.s + 1) >= steps) return x;  // no next step
     x.type = kItemGate;
     x.s += 1;
-    x.part = static_cast<int32_t>(j - ntt - 1);
+    x.part = static_cast<int32_t>(j - ntt);  // 1 .. P-1 (part 0 runs inside the DEC)
     return x;
   }
   // gate_done units before TILE(r, s) may run: INIT parts (+ NORM), then P per step
@@ -401,6 +404,12 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     csync();
     if (tid == 0) signal(c, 1);
   };
+  auto gate_part = [&](uint64_t r, int64_t s, int part, int cur) {  // spinmc.cpp:91-136 on 1/P of the groups
+    const GateRec& g = P.gates[static_cast<uint64_t>(s) * P.rows + r];
+    const int groups = G.n / 4, per = groups / static_cast<int>(q.P), g0 = part * per;
+    gate_pass(PX(r, cur), PY(r, cur), PX(r, cur ^ 1), PY(r, cur ^ 1), __ldg(&g.site), g, g0, g0 + per, tid, kThreads);
+    fence_proxy_async_global();  // psi' is read by the TMA engine
+  };
   auto run_control = [&](const Item& x) {
     const uint64_t r = x.r;
     if (x.type == kItemInit) {  // product_state / random_state amplitudes of part x.part
@@ -439,14 +448,7 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
         Q.row = load_row(&L.row[r]);
       }
       csync();
-      if (!Q.row.err) {
-        const int cur = Q.row.cur;
-        const GateRec& g = P.gates[static_cast<uint64_t>(x.s) * P.rows + r];
-        const int groups = G.n / 4, per = groups / static_cast<int>(q.P), g0 = x.part * per;
-        gate_pass(PX(r, cur), PY(r, cur), PX(r, cur ^ 1), PY(r, cur ^ 1), __ldg(&g.site), g, g0, g0 + per, tid,
-                  kThreads);
-        fence_proxy_async_global();  // psi' is read by the TMA engine
-      }
+      if (!Q.row.err) gate_part(r, x.s, x.part, Q.row.cur);
       sync_signal(&L.gate_done[r]);
       return;
     }
@@ -457,8 +459,10 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
       Q.row = load_row(&L.row[r]);
     }
     csync();
+    const bool next_gate = static_cast<uint64_t>(s + 1) < P.steps;
     if (Q.row.err) {
       sync_signal(&L.dec_done[r]);
+      if (next_gate && tid == 0) signal(&L.gate_done[r], 1);  // part 0 (no work)
       return;
     }
     // replay the per-thread chains of rho_partials_tma (CS = 1, tiles in ascending order)
@@ -546,6 +550,10 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     if (s >= 0 && !Q.row.err && P.renorm > 0 && (static_cast<uint64_t>(s) + 1) % P.renorm == 0)
       q_renormalize(G, PX(r, Q.row.cur), PY(r, Q.row.cur), tid, warp, lane, H);  // spinmc.cpp:246-248
     sync_signal(&L.dec_done[r]);
+    if (next_gate) {  // part 0 of the next step's gate, on the state just decided
+      if (!Q.row.err) gate_part(r, s + 1, 0, Q.row.cur);
+      sync_signal(&L.gate_done[r]);
+    }
   };
 
   // ------------------------------------------------------------------ consumer loop
