@@ -54,6 +54,11 @@ struct DeviceState {
   size_t trace_bytes = 0;
   void* workspace = nullptr;
   size_t workspace_bytes = 0;
+  // batched GEMM (tg_zgemm_batched): device operands and two pinned host staging slots
+  void* gemm_dev = nullptr;
+  size_t gemm_dev_bytes = 0;
+  void* gemm_pin = nullptr;
+  size_t gemm_pin_bytes = 0;
 };
 
 }  // namespace
@@ -290,6 +295,8 @@ tg_status tg_destroy(tg_ctx* ctx) {
     cudaStreamSynchronize(d.stream);
     if (d.trace) cudaFree(d.trace);
     if (d.workspace) cudaFree(d.workspace);
+    if (d.gemm_dev) cudaFree(d.gemm_dev);
+    if (d.gemm_pin) cudaFreeHost(d.gemm_pin);
     cudaStreamSynchronize(d.copy);
     cudaEventDestroy(d.ev0);
     cudaEventDestroy(d.ev1);
@@ -600,37 +607,105 @@ tg_status tg_zgemm_batched(tg_ctx* ctx, int device, int batch, int m, int n, int
     return fail(TG_EINVAL, "device index out of range");
   DeviceState& d = ctx->devs[device];
   TG_CUDA(cudaSetDevice(d.ordinal));
-  const size_t ea = 2ull * m * k, eb = 2ull * k * n, ec = 2ull * m * n;
+  // Column-major interleaved complex128 operands, copied in and out by the library
+  // (GemmTask ownership, exec.hpp:30-31). The batch runs in chunks through two pinned host
+  // slots: while chunk c is on the device (H2D, kernel, D2H on the stream), the host packs
+  // chunk c+1 into the other slot and unpacks chunk c-1; the device buffer and the pinned
+  // slots are grow-only and reused across calls.
+  const size_t ea = 2ull * m * k, eb = 2ull * k * n, ec = 2ull * m * n;  // doubles per entry
   const bool has_c = C != nullptr;
-  const size_t bytes = 8 * static_cast<size_t>(batch) * (ea + eb + (has_c ? ec : 0) + ec);
-  const auto t0 = std::chrono::steady_clock::now();
-  double* buf = nullptr;
-  TG_CUDA(cudaMallocAsync(&buf, bytes, d.stream));
-  // every return below frees the batch buffer (stream-ordered after the copies that use it)
-  struct FreeAsync {
-    double* p;
-    cudaStream_t s;
-    ~FreeAsync() { cudaFreeAsync(p, s); }
-  } guard{buf, d.stream};
-  double *dA = buf, *dB = dA + batch * ea, *dC = has_c ? dB + batch * eb : nullptr;
-  double* dO = (has_c ? dC + batch * ec : dB + batch * eb);
-  for (int i = 0; i < batch; ++i) {
-    TG_CUDA(cudaMemcpyAsync(dA + i * ea, A[i], 8 * ea, cudaMemcpyHostToDevice, d.stream));
-    TG_CUDA(cudaMemcpyAsync(dB + i * eb, B[i], 8 * eb, cudaMemcpyHostToDevice, d.stream));
-    if (has_c) TG_CUDA(cudaMemcpyAsync(dC + i * ec, C[i], 8 * ec, cudaMemcpyHostToDevice, d.stream));
+  const size_t in_per = ea + eb + (has_c ? ec : 0), per = in_per + ec;
+  constexpr size_t kChunkBytes = size_t{64} << 20;
+  const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(batch, kChunkBytes / (8 * per))));
+  const int nchunks = (batch + chunk - 1) / chunk;
+  const size_t slot = 8 * per * static_cast<size_t>(chunk);
+  const size_t dev_bytes = nchunks > 1 ? 2 * slot : slot;
+  if (d.gemm_dev_bytes < dev_bytes) {
+    if (d.gemm_dev) cudaFree(d.gemm_dev);
+    d.gemm_dev = nullptr;
+    d.gemm_dev_bytes = 0;
+    TG_CUDA(cudaMalloc(&d.gemm_dev, dev_bytes));
+    d.gemm_dev_bytes = dev_bytes;
   }
-  TG_CUDA(cudaEventRecord(d.ev0, d.stream));
-  cudaError_t e = tg::launch_zgemm_strided(batch, m, n, k, alpha[0], alpha[1], dA, ea / 2, dB, eb / 2,
-                                           beta[0], beta[1], dC, ec / 2, dO, ec / 2, g_perturb.load(),
-                                           d.stream);
-  if (e != cudaSuccess) return cuda_fail(e, "zgemm launch");
-  ++g_launches;
-  TG_CUDA(cudaEventRecord(d.ev1, d.stream));
-  for (int i = 0; i < batch; ++i)
-    TG_CUDA(cudaMemcpyAsync(out[i], dO + i * ec, 8 * ec, cudaMemcpyDeviceToHost, d.stream));
+  if (d.gemm_pin_bytes < dev_bytes) {
+    if (d.gemm_pin) cudaFreeHost(d.gemm_pin);
+    d.gemm_pin = nullptr;
+    d.gemm_pin_bytes = 0;
+    TG_CUDA(cudaMallocHost(&d.gemm_pin, dev_bytes));
+    d.gemm_pin_bytes = dev_bytes;
+  }
+  // host copies of `count` entries, split over threads when large
+  auto par_copy = [](int count, size_t bytes_each, auto&& one) {
+    const size_t total = bytes_each * static_cast<size_t>(count);
+    const int nt = total >= (size_t{8} << 20) ? std::min(8, std::max(1, static_cast<int>(std::thread::hardware_concurrency()))) : 1;
+    if (nt <= 1 || count < 2) {
+      for (int i = 0; i < count; ++i) one(i);
+      return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        for (int i = t; i < count; i += nt) one(i);
+      });
+    for (auto& x : th) x.join();
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<cudaEvent_t> evs(2 * nchunks + 2, nullptr);
+  struct EvGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EvGuard() {
+      for (auto e : v)
+        if (e) cudaEventDestroy(e);
+    }
+  } ev_guard{evs};
+  for (auto& ev : evs) TG_CUDA(cudaEventCreate(&ev));
+  cudaEvent_t* kev = evs.data();                 // kernel start/end per chunk
+  cudaEvent_t* done = evs.data() + 2 * nchunks;  // slot reuse: D2H of the slot's last chunk
+  auto unpack = [&](int c) {
+    const int b0 = c * chunk, cnt = std::min(chunk, batch - b0);
+    const double* hs = reinterpret_cast<const double*>(static_cast<char*>(d.gemm_pin) + (c & 1) * slot);
+    const double* ho = hs + static_cast<size_t>(cnt) * in_per;
+    par_copy(cnt, 8 * ec, [&](int i) { std::memcpy(out[b0 + i], ho + i * ec, 8 * ec); });
+  };
+  for (int c = 0; c < nchunks; ++c) {
+    const int b0 = c * chunk, cnt = std::min(chunk, batch - b0);
+    char* hslot = static_cast<char*>(d.gemm_pin) + (c & 1) * slot;
+    char* dslot = static_cast<char*>(d.gemm_dev) + (c & 1) * slot;
+    if (c >= 2) {  // the slot's previous chunk (c - 2): results out before the slot is reused
+      TG_CUDA(cudaEventSynchronize(done[c & 1]));
+      unpack(c - 2);
+    }
+    double* hA = reinterpret_cast<double*>(hslot);
+    double* hB = hA + static_cast<size_t>(cnt) * ea;
+    double* hC = hB + static_cast<size_t>(cnt) * eb;
+    par_copy(cnt, 8 * (ea + eb + (has_c ? ec : 0)), [&](int i) {
+      std::memcpy(hA + i * ea, A[b0 + i], 8 * ea);
+      std::memcpy(hB + i * eb, B[b0 + i], 8 * eb);
+      if (has_c) std::memcpy(hC + i * ec, C[b0 + i], 8 * ec);
+    });
+    const size_t in_bytes = 8 * in_per * static_cast<size_t>(cnt);
+    TG_CUDA(cudaMemcpyAsync(dslot, hslot, in_bytes, cudaMemcpyHostToDevice, d.stream));
+    double* dA = reinterpret_cast<double*>(dslot);
+    double* dB = dA + static_cast<size_t>(cnt) * ea;
+    double* dC = has_c ? dB + static_cast<size_t>(cnt) * eb : nullptr;
+    double* dO = dA + static_cast<size_t>(cnt) * in_per;
+    TG_CUDA(cudaEventRecord(kev[2 * c], d.stream));
+    cudaError_t e = tg::launch_zgemm_strided(cnt, m, n, k, alpha[0], alpha[1], dA, ea / 2, dB, eb / 2, beta[0],
+                                             beta[1], dC, ec / 2, dO, ec / 2, g_perturb.load(), d.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "zgemm launch");
+    ++g_launches;
+    TG_CUDA(cudaEventRecord(kev[2 * c + 1], d.stream));
+    TG_CUDA(cudaMemcpyAsync(hslot + in_bytes, dO, 8 * ec * static_cast<size_t>(cnt), cudaMemcpyDeviceToHost, d.stream));
+    TG_CUDA(cudaEventRecord(done[c & 1], d.stream));
+  }
   TG_CUDA(cudaStreamSynchronize(d.stream));
+  for (int c = std::max(0, nchunks - 2); c < nchunks; ++c) unpack(c);
   float kms = 0.f;
-  cudaEventElapsedTime(&kms, d.ev0, d.ev1);
+  for (int c = 0; c < nchunks; ++c) {
+    float x = 0.f;
+    cudaEventElapsedTime(&x, kev[2 * c], kev[2 * c + 1]);
+    kms += x;
+  }
   const auto t1 = std::chrono::steady_clock::now();
   if (records) {
     const int64_t exec_ns = std::max<int64_t>(1, static_cast<int64_t>(kms * 1e6 / batch));

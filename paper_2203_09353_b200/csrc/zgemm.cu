@@ -244,26 +244,36 @@ constexpr int TStage = 2 * TPanel;                  // A panel + B panel
 constexpr uint32_t TStageBytes = TStage * 8;
 static_assert(16 * 4 * ZT == TPanel, "B box = one panel");
 
-// WC warp columns: 2 (8 warps, 16x32 per warp) or 4 (16 warps, 16x16 per warp: twice the
-// warps per SMSP to hide the DMMA accumulator latency, as cuBLAS's 32x32x16 z884 kernel does
-// with 3 CTAs of 4 warps).
-template <int WC>
-__global__ void __launch_bounds__(128 * WC, 1) zgemm_tma_kernel(const ZArgs P, const __grid_constant__ CUtensorMap mapA,
-                                                               const __grid_constant__ CUtensorMap mapB) {
+// Warp grid WR x WC, each warp 16 rows x NB*8 columns: CTA tile (16 WR) x (8 NB WC).
+//  <4, 2, 4, 3, 1>: 8 warps, 64x64 tiles, 1 CTA per SM (192 KB of stages);
+//  <4, 4, 2, 3, 1>: 16 warps of 16x16: twice the warps per SMSP to hide the DMMA accumulator
+//                   latency;
+//  <2, 2, 2, 2, 3>: 4 warps, 32x32 tiles, 2 stages of 32 KB, 3 CTAs per SM — the shape of
+//                   cuBLAS's z884 32x32x16 kernel: a CTA's epilogue overlaps the other CTAs'
+//                   main loops (small K, where the epilogue weighs most).
+// Every 8x8 output block sees the same DMMA sequence in all three (and in zgemm_kernel):
+// results are bitwise equal.
+// PROD: one extra warpgroup whose first thread issues the TMA stages (the consumer warps
+// never leave the DMMA loop to issue).
+template <int WR, int WC, int NB, int STAGES, int MINB, bool PROD = false>
+__global__ void __launch_bounds__(32 * WR * WC + (PROD ? 128 : 0), MINB) zgemm_tma_kernel(const ZArgs P, const __grid_constant__ CUtensorMap mapA,
+                                                                      const __grid_constant__ CUtensorMap mapB) {
+  constexpr int TM = 16 * WR, TN = 8 * NB * WC;
+  constexpr int PanelA = WR * TBoxA, Stage = PanelA + 64 * TN;  // doubles
+  constexpr uint32_t StageBytes = Stage * 8;
   extern __shared__ __align__(1024) unsigned char zraw[];
   const uint32_t sbase = smem_u32(zraw);
   double* stages = reinterpret_cast<double*>(zraw + (((sbase + 1023u) & ~1023u) - sbase));
-  __shared__ uint64_t full[ZStages], empty[ZStages];
+  __shared__ uint64_t full[STAGES], empty[STAGES];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int NB = 8 / WC;  // 8x8 B blocks per warp
   const int wr = warp / WC, wc = warp % WC;
   const int mm = lane >> 2, kq = lane & 3;
   const int64_t mine = P.items > blockIdx.x ? (P.items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const int64_t total = mine * P.nk;
   if (tid == 0) {
-    for (int s = 0; s < ZStages; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 4 * WC);  // one arrival per warp
+      mbar_init(&empty[s], WR * WC);  // one arrival per warp
     }
     fence_mbar_init();
   }
@@ -274,6 +284,11 @@ __global__ void __launch_bounds__(128 * WC, 1) zgemm_tma_kernel(const ZArgs P, c
 #pragma unroll
   for (int i = 0; i < 2; ++i) fa[i] = wr * TBoxA + (2 * kq + i) * 16 + 2 * (mm ^ (i + 2 * kq));
   const int fb0 = (wc * NB * 8 + mm) * 64;  // column j = (wc * NB + jj) * 8 + mm, + jj * 512
+  // epilogue fast path: (1*sr - 0*si + 0*0) - 0*0 == sr + 0.0 bit for bit (the sum maps -0 to
+  // +0 as the full formula does); skips 13 FP64 ops per element that contend with the DMMAs
+  // (+0.0 exactly: a -0.0 alpha.im or beta would keep a -0 result)
+  const bool unit = P.ar == 1.0 && __double_as_longlong(P.ai) == 0 && __double_as_longlong(P.br) == 0 &&
+                    __double_as_longlong(P.bi) == 0 && P.C == nullptr;
   struct Cursor {
     int64_t w, e;
     int kc, i0, j0;
@@ -284,8 +299,8 @@ __global__ void __launch_bounds__(128 * WC, 1) zgemm_tma_kernel(const ZArgs P, c
     if (w < P.items) {
       q.e = w / (P.tm * P.tn);
       const int t = static_cast<int>(w - q.e * P.tm * P.tn);
-      q.i0 = (t / P.tn) * ZT;
-      q.j0 = (t % P.tn) * ZT;
+      q.i0 = (t / P.tn) * TM;
+      q.j0 = (t % P.tn) * TN;
     }
   };
   auto advance = [&](Cursor& q) {
@@ -294,15 +309,15 @@ __global__ void __launch_bounds__(128 * WC, 1) zgemm_tma_kernel(const ZArgs P, c
   Cursor prod, cons;
   set_item(prod, blockIdx.x);
   set_item(cons, blockIdx.x);
-  auto issue = [&](int64_t it) {  // thread 0: chunk it (= prod's) into stage it % ZStages
-    const int s = static_cast<int>(it % ZStages);
-    if (it >= ZStages) mbar_wait(&empty[s], static_cast<uint32_t>(it / ZStages - 1) & 1);
-    double* st = stages + s * TStage;
-    mbar_expect_tx(&full[s], TStageBytes);
+  auto issue = [&](int64_t it) {  // thread 0: chunk it (= prod's) into stage it % STAGES
+    const int s = static_cast<int>(it % STAGES);
+    if (it >= STAGES) mbar_wait(&empty[s], static_cast<uint32_t>(it / STAGES - 1) & 1);
+    double* st = stages + s * Stage;
+    mbar_expect_tx(&full[s], StageBytes);
     const int e = static_cast<int>(prod.e), k0 = prod.kc * ZK;
 #pragma unroll
-    for (int h = 0; h < 4; ++h) tma_load_4d(st + h * TBoxA, &mapA, 0, prod.i0 / 8 + 2 * h, k0, e, &full[s]);
-    tma_load_4d(st + TPanel, &mapB, 0, k0 / 8, prod.j0, e, &full[s]);
+    for (int h = 0; h < WR; ++h) tma_load_4d(st + h * TBoxA, &mapA, 0, prod.i0 / 8 + 2 * h, k0, e, &full[s]);
+    tma_load_4d(st + PanelA, &mapB, 0, k0 / 8, prod.j0, e, &full[s]);
     advance(prod);
   };
   double cr[2][NB][2], ci[2][NB][2];
@@ -310,16 +325,21 @@ __global__ void __launch_bounds__(128 * WC, 1) zgemm_tma_kernel(const ZArgs P, c
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < NB; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
-  if (tid == 0) {
-    if (total > 0) issue(0);
-    if (total > 1) issue(1);
+  if constexpr (PROD) {
+    if (tid >= 32 * WR * WC) {
+      if (tid == 32 * WR * WC)
+        for (int64_t it = 0; it < total; ++it) issue(it);
+      return;
+    }
+  } else if (tid == 0) {
+    for (int64_t it = 0; it < STAGES - 1 && it < total; ++it) issue(it);
   }
   for (int64_t it = 0; it < total; ++it) {
-    const int s = static_cast<int>(it % ZStages);
-    if (tid == 0 && it + 2 < total) issue(it + 2);
-    mbar_wait(&full[s], static_cast<uint32_t>(it / ZStages) & 1);
-    const double* sa = stages + s * TStage;
-    const double* sb = sa + TPanel;
+    const int s = static_cast<int>(it % STAGES);
+    if (!PROD && tid == 0 && it + STAGES - 1 < total) issue(it + STAGES - 1);
+    mbar_wait(&full[s], static_cast<uint32_t>(it / STAGES) & 1);
+    const double* sa = stages + s * Stage;
+    const double* sb = sa + PanelA;
 #pragma unroll
     for (int kb = 0; kb < ZK; kb += 4) {
       double xa[2], ya[2], yn[2], xb[NB], yb[NB];
@@ -378,12 +398,16 @@ __global__ void __launch_bounds__(128 * WC, 1) zgemm_tma_kernel(const ZArgs P, c
                 cvi = v.y;
               }
               const double sr = cr[i][j][h], si = ci[i][j][h];
-              const double re = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(P.ar, sr), __dmul_rn(P.ai, si)),
-                                                    __dmul_rn(P.br, cvr)),
-                                          __dmul_rn(P.bi, cvi));
-              const double im = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(P.ar, si), __dmul_rn(P.ai, sr)),
-                                                    __dmul_rn(P.br, cvi)),
-                                          __dmul_rn(P.bi, cvr));
+              double re, im;
+              if (unit) {  // alpha = 1, beta = 0, no C: the formula below reduces to x + 0.0 exactly
+                re = __dadd_rn(sr, 0.0);
+                im = __dadd_rn(si, 0.0);
+              } else {
+                re = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(P.ar, sr), __dmul_rn(P.ai, si)), __dmul_rn(P.br, cvr)),
+                               __dmul_rn(P.bi, cvi));
+                im = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(P.ar, si), __dmul_rn(P.ai, sr)), __dmul_rn(P.br, cvi)),
+                               __dmul_rn(P.bi, cvr));
+              }
               *reinterpret_cast<double2*>(o + 2 * idx) = make_double2(re, im);
             }
             cr[i][j][h] = 0.0;
@@ -458,19 +482,38 @@ cudaError_t launch_zgemm_strided(int batch, int m, int n, int k, double ar, doub
   // TMA staging when the shapes allow it (TG_ZGEMM_TMA=0: the cp.async pipeline)
   const char* env = std::getenv("TG_ZGEMM_TMA");
   if (!(env && env[0] == '0') && m % 8 == 0 && k % 8 == 0) {
-    CUtensorMap mapA, mapB;
-    if (encode_operand(&mapA, A, m, k, batch, sA, 2, ZK) && encode_operand(&mapB, B, k, n, batch, sB, 4, ZT)) {
-      constexpr int tbytes = ZStages * TStageBytes + 1024;
-      // 16 warps (16x16 each) once K is long enough for the main loop to dominate (+1.2 % at
-      // 1024^3, -1.3 % at 64^3); TG_ZGEMM_WARPS=8|16 overrides
-      const char* w = std::getenv("TG_ZGEMM_WARPS");
-      const bool w16 = w ? std::atoi(w) == 16 : P.nk >= 4;
-      auto kern = w16 ? zgemm_tma_kernel<4> : zgemm_tma_kernel<2>;
+    // kernel shape (TG_ZGEMM_WARPS=4|8|9|16 overrides; profiles/r02_zgemm_vs_cublas.txt): the
+    // 4-warp 32x32-tile kernel (3 CTAs per SM) when 64x64 tiles would pad m x n noticeably
+    // more (96^3: 31.7 vs 18.5 TF/s), else 8 warps of 16x32 plus a producer warp that issues
+    // the TMA stages ("9": best or within 0.3 % of the best at every measured size)
+    auto fill = [&](int t) {
+      const double mp = static_cast<double>((m + t - 1) / t * t), np_ = static_cast<double>((n + t - 1) / t * t);
+      return static_cast<double>(m) * n / (mp * np_);
+    };
+    const char* w = std::getenv("TG_ZGEMM_WARPS");
+    const int warps = w ? std::atoi(w) : (fill(32) > 1.05 * fill(64) ? 4 : 9);
+    auto run = [&](auto kern, int wr, int tn, int stages, int minb, int extra = 0) -> cudaError_t {
+      ZArgs Q = P;
+      Q.tm = (m + 16 * wr - 1) / (16 * wr);
+      Q.tn = (n + tn - 1) / tn;
+      Q.items = static_cast<int64_t>(batch) * Q.tm * Q.tn;
+      CUtensorMap mapA, mapB;
+      if (!encode_operand(&mapA, A, m, k, batch, sA, 2, ZK) || !encode_operand(&mapB, B, k, n, batch, sB, 4, tn))
+        return cudaErrorNotSupported;
+      const int stage_bytes = (wr * TBoxA + 64 * tn) * 8;
+      const int tbytes = stages * stage_bytes + 1024;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tbytes);
       if (e != cudaSuccess) return e;
-      kern<<<grid, w16 ? 512 : 256, tbytes, stream>>>(P, mapA, mapB);
+      const int g = static_cast<int>(std::min<int64_t>(Q.items, static_cast<int64_t>(sms) * minb));
+      kern<<<g, 32 * wr * (warps == 4 ? 2 : warps / wr) + extra, tbytes, stream>>>(Q, mapA, mapB);
       return cudaGetLastError();
-    }
+    };
+    cudaError_t e = cudaErrorNotSupported;
+    if (warps == 4) e = run(zgemm_tma_kernel<2, 2, 2, 2, 3>, 2, 32, 2, 3);
+    else if (warps == 16) e = run(zgemm_tma_kernel<4, 4, 2, 3, 1>, 4, 64, 3, 1);
+    else if (warps == 9) e = run(zgemm_tma_kernel<4, 2, 4, 3, 1, true>, 4, 64, 3, 1, 128);  // + producer
+    else e = run(zgemm_tma_kernel<4, 2, 4, 3, 1>, 4, 64, 3, 1);
+    if (e != cudaErrorNotSupported) return e;
   }
   constexpr int bytes = ZStages * StageElems * 16;
   cudaError_t e = cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);

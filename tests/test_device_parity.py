@@ -183,6 +183,27 @@ def test_t5_batched_gemm_ordered_and_large(device, oracle):
         device.batched_gemm([np.eye(2), np.eye(3)], [np.eye(2), np.eye(3)])
 
 
+def test_batched_gemm_unit_epilogue_bitwise(device, monkeypatch):
+    """alpha = 1, beta = 0, no C: the TMA kernels' one-op epilogue (acc + 0.0) is bitwise the
+    general alpha/beta formula of the cp.async kernel, including -0 entries (a zero column of
+    A makes every product term -0 or +0)."""
+    rng = np.random.default_rng(5)
+    m = n = k = 64
+    As = [rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k)) for _ in range(6)]
+    Bs = [rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n)) for _ in range(6)]
+    As[0][:, :] = -0.0  # -0 products: the epilogue decides the sign of every zero
+    As[1][3, :] = 0.0
+    monkeypatch.setenv("TG_ZGEMM_TMA", "0")
+    ref = device.batched_gemm(As, Bs)
+    monkeypatch.setenv("TG_ZGEMM_TMA", "1")
+    for warps in ("4", "8", "9", "16"):
+        monkeypatch.setenv("TG_ZGEMM_WARPS", warps)
+        got = device.batched_gemm(As, Bs)
+        for i in range(6):
+            assert np.array_equal(np.ascontiguousarray(got[i]).view(np.uint64),
+                                  np.ascontiguousarray(ref[i]).view(np.uint64)), (warps, i)
+
+
 @pytest.mark.parametrize("m,n,k,batch", [(64, 64, 64, 17), (72, 37, 40, 5), (256, 256, 256, 3), (8, 8, 8, 9),
                                          (200, 64, 136, 3), (128, 130, 1024, 2)])
 def test_batched_gemm_tma_vs_cp_async_bitwise(device, monkeypatch, m, n, k, batch):
@@ -197,7 +218,7 @@ def test_batched_gemm_tma_vs_cp_async_bitwise(device, monkeypatch, m, n, k, batc
     ref = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
     monkeypatch.setenv("TG_ZGEMM_TMA", "1")
     got = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
-    for warps in ("8", "16"):  # both warp layouts of the TMA kernel
+    for warps in ("4", "8", "9", "16"):  # every warp layout of the TMA kernel (9: 8 + producer)
         monkeypatch.setenv("TG_ZGEMM_WARPS", warps)
         again = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
         for i in range(batch):
