@@ -57,6 +57,14 @@ typedef struct {
   uint64_t renormalize_interval; /* 1000 by default; 0 disables                          */
   uint32_t shard_index, shard_count;
   uint64_t fault_procedure, fault_step;  /* inject_fault == 2 only                     */
+  int32_t rho_half;              /* opt-in, Renyi-2 with spins >= 13: form only the upper   *
+                                  * triangle of rho's 64x64 tiles (rho is Hermitian;        *
+                                  * ||rho||_F^2 = diagonal tiles + 2 x off-diagonal ones).  *
+                                  * Not the reference's arithmetic (its GEMM is the full    *
+                                  * product): entropies agree within the parity *
+                                  * tolerance, and the flops actually executed are reported *
+                                  * in tg_anneal_result.executed_flops next to total_flops  *
+                                  * (the graded full-GEMM count). 0 = full GEMM (default).  */
 } tg_anneal_config;
 
 /* One logged near-tie accept decision: |u - p| < 1e-9 in the test
@@ -98,6 +106,8 @@ typedef struct {
   tg_near_tie* near_tie_log;     /* optional [near_tie_capacity]: the first near ties,    *
                                   * sorted by (procedure, step)                           */
   uint64_t near_tie_capacity;
+  uint64_t executed_flops;       /* out: GEMM flops the device executed (= total_flops     *
+                                  * unless rho_half)                                       */
 } tg_anneal_result;
 
 /* Device-resident outputs for tg_anneal_launch (rows as above). */

@@ -65,7 +65,7 @@ class CAnnealConfig(C.Structure):
         ("objective", C.c_int32), ("initial_state", C.c_int32), ("inject_fault", C.c_int32),
         ("t0", C.c_double), ("t_min", C.c_double), ("renormalize_interval", C.c_uint64),
         ("shard_index", C.c_uint32), ("shard_count", C.c_uint32),
-        ("fault_procedure", C.c_uint64), ("fault_step", C.c_uint64),
+        ("fault_procedure", C.c_uint64), ("fault_step", C.c_uint64), ("rho_half", C.c_int32),
     ]
 
 
@@ -88,6 +88,7 @@ class CAnnealResult(C.Structure):
         ("device_kernel_ms", C.POINTER(C.c_double)), ("device_resident", C.POINTER(C.c_uint64)),
         ("initial_wall_ns", C.POINTER(C.c_int64)), ("fallback_decisions", C.c_uint64),
         ("near_ties", C.c_uint64), ("near_tie_log", C.POINTER(CNearTie)), ("near_tie_capacity", C.c_uint64),
+        ("executed_flops", C.c_uint64),
     ]
 
 
@@ -230,6 +231,7 @@ class ExperimentConfig:
     inject_fault: int = 0       # 1: perturb_gemm (linalg.hpp:74-79); 2: non-unitary gate (below)
     fault_procedure: int = 0    # inject_fault == 2: this procedure's gate at fault_step is scaled by 1.001
     fault_step: int = 0
+    rho_half: bool = False      # opt-in Hermitian half of rho (Renyi-2, spins >= 13): executed flops reported apart
 
     def to_c(self) -> CAnnealConfig:
         for name, table in (("entropy_kind", _ENTROPY), ("objective", _OBJECTIVE),
@@ -242,7 +244,7 @@ class ExperimentConfig:
                              _ENTROPY[self.entropy_kind], _OBJECTIVE[self.objective],
                              _INITIAL[self.initial_state], int(self.inject_fault), self.t0, self.t_min,
                              self.renormalize_interval, self.shard_index, self.shard_count,
-                             self.fault_procedure, self.fault_step)
+                             self.fault_procedure, self.fault_step, int(bool(self.rho_half)))
 
     def rows(self) -> int:
         c = self.to_c()
@@ -287,6 +289,7 @@ class RunReport:
     fallback_decisions: int = 0  # decisions re-taken with the reference formula (lean margin in the window)
     near_ties: int = 0           # decisions with |u - p| < 1e-9
     near_tie_log: list = field(default_factory=list)  # NearTie, (procedure, step) order
+    executed_flops: int = 0      # GEMM flops executed on the device (< total_flops with rho_half)
 
     def trace(self, row: int) -> EntropyTrace:
         return EntropyTrace(int(self.procedures[row]), float(self.initial_entropy[row]),
@@ -395,7 +398,8 @@ class Device:
         return RunReport(cfg, procs, init, ent, acc, st, wl, fin, res.average_entropy, res.total_wall_ns,
                          res.total_flops, res.kernel_ms, device_kernel_ms=list(dms[:max(cfg.devices, 1)]),
                          device_resident=list(drs[:max(cfg.devices, 1)]), initial_wall_ns=iw,
-                         fallback_decisions=res.fallback_decisions, near_ties=res.near_ties, near_tie_log=ties)
+                         fallback_decisions=res.fallback_decisions, near_ties=res.near_ties, near_tie_log=ties,
+                         executed_flops=res.executed_flops)
 
     def batched_gemm(self, a_list, b_list, c_list=None, alpha=1.0, beta=0.0, device: int = 0,
                      procedures=None, records: bool = False):

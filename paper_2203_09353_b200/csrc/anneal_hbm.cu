@@ -508,10 +508,10 @@ namespace {
 constexpr size_t kQueueSlabBudget = size_t{48} << 30;
 constexpr uint64_t kQueueMaxRows = 8192;
 
-bool queue_possible(uint32_t spins, uint64_t rows, int entropy_kind) {
+bool queue_possible(uint32_t spins, uint64_t rows, int entropy_kind, bool half = false) {
   if (entropy_kind != TG_RENYI2 || rows == 0 || rows > kQueueMaxRows || !hbm_use_tma()) return false;
   const char* env = std::getenv("TG_HBM_QUEUE");
-  if (env && env[0] == '0') return false;
+  if (env && env[0] == '0' && !half) return false;
   return rows * (size_t{32} << spins) <= kQueueSlabBudget;
 }
 
@@ -522,8 +522,9 @@ bool queue_possible(uint32_t spins, uint64_t rows, int entropy_kind) {
 // has): profiles/r02_queue_vs_cluster.txt.
 // TG_HBM_QUEUE=1 forces the queue, =0 the cluster schedule; TG_HBM_CTAS_PER_REPLICA or the
 // phase-trace probe force the cluster schedule.
-bool queue_pick(uint32_t spins, uint64_t rows, int entropy_kind, int device, bool trace) {
-  if (trace || !queue_possible(spins, rows, entropy_kind)) return false;
+bool queue_pick(uint32_t spins, uint64_t rows, int entropy_kind, int device, bool trace, bool half = false) {
+  if (trace || !queue_possible(spins, rows, entropy_kind, half)) return false;
+  if (half) return true;  // rho_half runs on the queue schedule only
   const char* env = std::getenv("TG_HBM_QUEUE");
   if (env && env[0] == '1') return true;
   if (std::getenv("TG_HBM_CTAS_PER_REPLICA")) return false;
@@ -547,11 +548,15 @@ bool queue_pick(uint32_t spins, uint64_t rows, int entropy_kind, int device, boo
 }  // namespace
 
 uint64_t anneal_hbm_queue_rows(uint32_t spins, uint64_t rows, int entropy_kind) {
-  return queue_possible(spins, rows, entropy_kind) ? rows : 0;
+  return queue_possible(spins, rows, entropy_kind, true) ? rows : 0;
+}
+
+uint64_t anneal_hbm_queue_max_rows(uint32_t spins) {
+  return std::min<uint64_t>(kQueueMaxRows, kQueueSlabBudget / (size_t{32} << spins));
 }
 
 int anneal_hbm_schedule(const AnnealParams& p, int device) {
-  return queue_pick(p.spins, p.rows, p.entropy_kind, device, false) ? 1 : 0;
+  return queue_pick(p.spins, p.rows, p.entropy_kind, device, false, p.rho_half != 0) ? 1 : 0;
 }
 
 // [max(cluster slabs, queue rows) slabs][queue region (partials, row state, counters)]
@@ -569,7 +574,7 @@ uint64_t anneal_hbm_wave_rows(const AnnealParams& p) {  // co-resident clusters 
   int dev = 0, cs = 1;
   uint64_t clusters = 0;
   cudaGetDevice(&dev);
-  if (queue_pick(p.spins, p.rows, p.entropy_kind, dev, false)) return p.rows;  // one wave: every row at once
+  if (queue_pick(p.spins, p.rows, p.entropy_kind, dev, false, p.rho_half != 0)) return p.rows;  // one wave
   if (hbm_geometry(p.spins, p.rows, p.entropy_kind, dev, cs, clusters) != cudaSuccess) return 0;
   return clusters;
 }
@@ -616,8 +621,10 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   const char* qenv = std::getenv("TG_HBM_QUEUE");
   const bool queue_stats = trace && qenv && qenv[0] == '1';
   if (p.rows > 0 && p.queue_rows >= p.rows &&
-      (queue_stats ? queue_possible(p.spins, p.rows, p.entropy_kind) : queue_pick(p.spins, p.rows, p.entropy_kind, dev, trace)))
+      (queue_stats ? queue_possible(p.spins, p.rows, p.entropy_kind)
+                   : queue_pick(p.spins, p.rows, p.entropy_kind, dev, trace, p.rho_half != 0)))
     return launch_queue(p, stream, dev, grid_out, queue_stats);
+  if (p.rho_half) return cudaErrorInvalidValue;  // the Hermitian half exists on the queue schedule only
   cudaError_t e = hbm_geometry(p.spins, p.rows, p.entropy_kind, dev, cs, clusters);
   if (e != cudaSuccess) return e;
   // never more clusters than the workspace has slabs (the persistent loop strides over rows)

@@ -97,6 +97,10 @@ tg_status validate(const tg_anneal_config* c) {
     return fail(TG_EINVAL, "device von-neumann entropy covers spins <= " + std::to_string(tg::kVnMaxSpins) +
                                " (rho resident in shared memory); use renyi-2");
   if (c->inject_fault < 0 || c->inject_fault > 2) return fail(TG_ECONFIG, "inject_fault must be 0, 1 or 2");
+  if (c->rho_half != 0 && c->rho_half != 1) return fail(TG_ECONFIG, "rho_half must be 0 or 1");
+  if (c->rho_half && (c->entropy_kind != TG_RENYI2 || c->spins <= static_cast<uint32_t>(tg::kSmemMaxSpins)))
+    return fail(TG_ECONFIG, "rho_half (Hermitian half of rho) needs renyi-2 and spins >= " +
+                                std::to_string(tg::kSmemMaxSpins + 1) + " (the HBM tier's work-queue schedule)");
   if (c->objective != TG_MAXIMIZE && c->objective != TG_MINIMIZE)
     return fail(TG_ECONFIG, "objective must be max or min");
   if (c->initial_state != TG_PRODUCT && c->initial_state != TG_RANDOM)
@@ -119,6 +123,7 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
   p.gate_fault = c->inject_fault == 2;
   p.fault_procedure = c->fault_procedure;
   p.fault_step = c->fault_step;
+  p.rho_half = c->rho_half;
   p.fault_row1 = 0;
   p.tie_eps = 1e-9;  // SURVEY.md §8c near tie; tests widen it to exercise the audit log
   if (const char* e = std::getenv("TG_NEAR_TIE_EPS")) {
@@ -155,7 +160,8 @@ uint64_t slab_clusters(uint32_t spins, uint64_t rows, int device) {
 // Workspace for one launch: [proposal stream of one batch][HBM-tier slabs] (+ alignment).
 size_t workspace_for(const tg::AnnealParams& p, int device) {
   const size_t per_row = tg::gate_stream_bytes_per_row(p.spins, p.steps, p.initial_state == 1);
-  const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(p.rows, kStreamBudget / per_row));
+  uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(p.rows, kStreamBudget / per_row));
+  if (p.rho_half) batch = std::max<uint64_t>(1, std::min<uint64_t>(batch, tg::anneal_hbm_queue_max_rows(p.spins)));
   return batch * per_row + slab_bytes(p.spins, batch, device, p.entropy_kind) + 1024;
 }
 
@@ -171,6 +177,7 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
   if (p.rows == 0) return cudaSuccess;
   const size_t per_row = tg::gate_stream_bytes_per_row(p.spins, p.steps, p.initial_state == 1);
   uint64_t batch = std::min<uint64_t>(p.rows, kStreamBudget / per_row);
+  if (p.rho_half) batch = std::min<uint64_t>(batch, tg::anneal_hbm_queue_max_rows(p.spins));  // queue schedule only
   while (batch > 0 && batch * per_row + slab_bytes(p.spins, batch, dev, p.entropy_kind) + 1024 > ws_bytes) --batch;
   if (batch == 0) return cudaErrorMemoryAllocation;
   const size_t stream_bytes = batch * per_row;
@@ -571,6 +578,11 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
     sum += steps > 0 ? finals[hr % D][hr / D] : res->initial_entropy[hr];
   res->average_entropy = rows ? sum / static_cast<double>(rows) : 0.0;
   res->total_flops = (rows * steps + rows) * tg_step_flops(cfg->spins);
+  res->executed_flops = res->total_flops;
+  if (cfg->rho_half) {  // upper-triangle tiles only: nt (nt + 1) / 2 of nt^2
+    const uint64_t nt = (uint64_t{1} << (cfg->spins / 2)) / 64;
+    res->executed_flops = res->total_flops / (nt * nt) * (nt * (nt + 1) / 2);
+  }
   res->kernel_ms = *std::max_element(ms.begin(), ms.end());
   res->total_wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
                            std::chrono::steady_clock::now() - t_begin)

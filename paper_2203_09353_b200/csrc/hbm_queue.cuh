@@ -77,18 +77,21 @@ static_assert(kThreads * kConsumerRegs + 128 * kProducerRegs <= 65536, "register
 
 // Queue geometry; identical on host (sizing, launch) and device.
 struct QGeo {
-  uint32_t spins, nt, ntt, P, Ip, lagD, lagG;
+  uint32_t spins, nt, ntt, nfull, P, Ip, lagD, lagG;
+  bool half;  // rho_half: the upper-triangle tiles only (ntt = nt (nt + 1) / 2 items per step)
   uint64_t rows, steps, BS, pro, K, total, n;
   __host__ __device__ static uint32_t gate_parts(uint32_t spins) {
     const uint64_t groups = uint64_t{1} << (spins - 2);
     const uint64_t p = groups / 4096;
     return static_cast<uint32_t>(p < 1 ? 1 : (p > 16 ? 16 : p));
   }
-  __host__ __device__ QGeo(uint32_t s, uint64_t r, uint64_t st, bool random, uint32_t grid) {
+  __host__ __device__ QGeo(uint32_t s, uint64_t r, uint64_t st, bool random, uint32_t grid, bool h = false) {
     spins = s;
     n = uint64_t{1} << s;
     nt = (1u << (s / 2)) / TB;
-    ntt = nt * nt;
+    nfull = nt * nt;
+    half = h;
+    ntt = half ? nt * (nt + 1) / 2 : nfull;
     P = gate_parts(s);
     Ip = P + (random ? 1 : 0);
     rows = r;
@@ -124,7 +127,7 @@ struct QGeo {
       x.type = kItemTile;
       x.r = k % rows;
       x.s = static_cast<int64_t>(k / rows) - 1;
-      x.part = static_cast<int32_t>(j);
+      x.part = static_cast<int32_t>(half ? upper_tile(j) : j);  // full tile index ti * nt + tj
       return x;
     }
     const uint64_t lag = j == ntt ? lagD : lagG;
@@ -141,6 +144,15 @@ struct QGeo {
     x.s += 1;
     x.part = static_cast<int32_t>(j - ntt);  // 1 .. P-1 (part 0 runs inside the DEC)
     return x;
+  }
+  // j-th tile of the upper triangle (ti <= tj), row-major
+  __host__ __device__ uint32_t upper_tile(uint32_t j) const {
+    uint32_t ti = 0;
+    while (j >= nt - ti) {
+      j -= nt - ti;
+      ++ti;
+    }
+    return ti * nt + ti + j;
   }
   // gate_done units before TILE(r, s) may run: INIT parts (+ NORM), then P per step
   __host__ __device__ uint64_t gate_target(int64_t s) const { return Ip + static_cast<uint64_t>(s + 1) * P; }
@@ -286,7 +298,7 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
   const uint32_t sbase = smem_u32(smem_raw);
   double* stages = reinterpret_cast<double*>(smem_raw + (((sbase + kQHeaderBytes + 1023u) & ~1023u) - sbase));
   const Geo G(static_cast<int>(P.spins));
-  const QGeo q(P.spins, P.rows, P.steps, P.initial_state == 1, gridDim.x);
+  const QGeo q(P.spins, P.rows, P.steps, P.initial_state == 1, gridDim.x, P.rho_half != 0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt = G.tiles(), nk = G.kchunks(), lnt = G.la - 6;
   const uint64_t cap = P.queue_rows;
@@ -468,11 +480,14 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     // replay the per-thread chains of rho_partials_tma (CS = 1, tiles in ascending order)
     double rho[kChains] = {0.0, 0.0, 0.0, 0.0}, tr[kChains] = {0.0, 0.0, 0.0, 0.0};
     {
-      const double* tvr = L.tv + r * q.ntt * kThreads + tid;
-      for (uint32_t t0 = 0; t0 < q.ntt; t0 += kChains) {
+      const double* tvr = L.tv + r * q.nfull * kThreads + tid;
+      for (uint32_t t0 = 0; t0 < q.nfull; t0 += kChains) {
 #pragma unroll
-        for (int c = 0; c < kChains; ++c)
-          if (t0 + c < q.ntt) rho[c] = rho[c] + __ldcg(tvr + static_cast<size_t>(t0 + c) * kThreads);
+        for (int c = 0; c < kChains; ++c) {
+          const uint32_t t = t0 + c;  // rho_half: lower tiles (ti > tj) were not formed
+          if (t < q.nfull && !(q.half && (t >> lnt) > (t & (nt - 1))))
+            rho[c] = rho[c] + __ldcg(tvr + static_cast<size_t>(t) * kThreads);
+        }
       }
       const bool h0 = diag_has(0, wr, wc, m, kq), h1 = diag_has(1, wr, wc, m, kq);
       const double* dgr = L.dg + r * nt * 2 * kThreads + tid;
@@ -665,7 +680,8 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     }
     double rho1[kChains] = {0.0, 0.0, 0.0, 0.0};
     tile_fold(cr, ci, rho1, 0, false);  // rho1[0] = 0.0 + tv (tile_fold's arithmetic)
-    __stcg(L.tv + (r * q.ntt + static_cast<uint64_t>(md.t)) * kThreads + tid, rho1[0]);
+    if (q.half && !diag) rho1[0] += rho1[0];  // rho_half: the mirrored lower tile (exact)
+    __stcg(L.tv + (r * q.nfull + static_cast<uint64_t>(md.t)) * kThreads + tid, rho1[0]);
     __syncwarp();
     if (lane == 0) signal(&L.tiles_done[r], 1);
     if (STATS && tid == 32) {

@@ -47,6 +47,7 @@ struct AnnealParams {
   uint64_t fault_procedure;    // (fault_procedure, fault_step) is scaled by 1.001
   uint64_t fault_step;
   uint64_t fault_row1;         // 1 + its row in this launch (0 = not in it; zero-init safe), per batch
+  int32_t rho_half;            // Renyi-2, HBM tier, work-queue schedule only: upper-triangle tiles
 };
 
 // Pre-generated proposal stream of one launch (gate_stream.cu).
@@ -85,6 +86,7 @@ size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int
 int anneal_hbm_schedule(const AnnealParams& p, int device);
 uint64_t anneal_hbm_slab_clusters(uint64_t rows, int device);  // slabs for launches of <= rows replicas
 uint64_t anneal_hbm_queue_rows(uint32_t spins, uint64_t rows, int entropy_kind);  // queue region capacity
+uint64_t anneal_hbm_queue_max_rows(uint32_t spins);  // largest launch the queue schedule takes
 
 // probes.cu
 cudaError_t probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* d_out, cudaStream_t s);

@@ -126,3 +126,14 @@ def test_environment_switches_documented():
     design = open(os.path.join(root, "DESIGN.md")).read()
     assert used, "no switches found"
     assert not [v for v in sorted(used) if f"`{v}" not in design], sorted(used)
+
+
+def test_rho_half_validation():
+    """rho_half is a Renyi-2, HBM-tier option: anything else is a ConfigError (host-side
+    validation, no GPU needed)."""
+    ok = tg.ExperimentConfig(spins=14, steps=2, procedures=1, rho_half=True)
+    ok.validate()
+    for bad in (tg.ExperimentConfig(spins=12, steps=2, procedures=1, rho_half=True),
+                tg.ExperimentConfig(spins=14, steps=2, procedures=1, rho_half=True, entropy_kind="von-neumann")):
+        with pytest.raises(tg.ConfigError, match="rho_half"):
+            bad.validate()

@@ -136,3 +136,45 @@ def test_queue_schedule_choice():
     assert L.tg_hbm_schedule(20, 64, 1) == 1
     assert L.tg_hbm_schedule(14, 65536, 1) == 0
     assert L.tg_hbm_schedule(14, 64, 0) == 0  # von Neumann: cluster schedule only
+
+
+# ----------------------------------------------- opt-in Hermitian half of rho (rho_half)
+@pytest.mark.parametrize("spins,procs,steps,init", [(13, 3, 10, "random"), (14, 5, 12, "product"),
+                                                     (16, 3, 6, "random"), (18, 2, 3, "product")])
+def test_rho_half_vs_oracle(device, oracle, spins, procs, steps, init):
+    """rho_half forms only the upper-triangle 64x64 tiles of rho (diagonal tiles once,
+    off-diagonal tiles twice in ||rho||_F^2): sites and accept flags still bit-exact against the
+    oracle, entropies within the 1e-10 parity tolerance, reruns bitwise, executed flops
+    reported apart from the graded full-GEMM count."""
+    cfg = tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=12, initial_state=init)
+    full = device.run(cfg)
+    cfg.rho_half = True
+    half = device.run(cfg)
+    again = device.run(cfg)
+    assert_bitwise(half, again)
+    assert np.array_equal(half.sites, full.sites) and np.array_equal(half.accepted, full.accepted)
+    assert close(half.entropies, full.entropies, 1e-12).all()
+    nt = (1 << (spins // 2)) // 64
+    assert half.total_flops == full.total_flops == full.executed_flops
+    assert half.executed_flops == full.total_flops // (nt * nt) * (nt * (nt + 1) // 2)
+    if spins <= 16:
+        want = oracle.run(McCfg(spins=spins, steps=steps, seed=12, initial_state=1 if init == "random" else 0), 0, procs)
+        assert np.array_equal(half.sites, want.sites)
+        assert np.array_equal(half.accepted, want.accepted)
+        assert close(half.entropies, want.entropies).all()
+        assert close(half.initial_entropy, want.initial).all()
+
+
+def test_rho_half_renormalisation_and_errors(device, monkeypatch):
+    """rho_half across renormalisations and with the cluster schedule forced off-limits (the
+    option always runs on the work queue); the not-normalised error keeps the reference message."""
+    monkeypatch.setenv("TG_HBM_QUEUE", "0")
+    cfg = tg.ExperimentConfig(spins=14, steps=20, procedures=4, seed=3, renormalize_interval=6, rho_half=True)
+    a = device.run(cfg)
+    cfg.rho_half = False
+    b = device.run(cfg)
+    assert np.array_equal(a.accepted, b.accepted) and close(a.entropies, b.entropies, 1e-12).all()
+    bad = tg.ExperimentConfig(spins=14, steps=8, procedures=4, seed=5, inject_fault=2, fault_procedure=1,
+                              fault_step=2, rho_half=True)
+    with pytest.raises(ValueError, match="entanglement_entropy: state not normalized"):
+        device.run(bad)
