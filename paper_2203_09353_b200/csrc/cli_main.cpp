@@ -65,7 +65,7 @@ struct Options {
   std::string mode = "device", device_mode = "shared", entropy = "renyi-2", objective = "max",
               initial_state = "product";
   double t0 = 1.0, t_min = 1e-3;
-  bool seed_given = false, kernel_log = false;
+  bool seed_given = false, kernel_log = false, rho_half = false;
   std::vector<uint64_t> sweep;
   uint64_t repeats = 3;
   std::string baseline, out_dir = ".";
@@ -113,6 +113,7 @@ tg_anneal_config to_config(const Options& o) {
   c.t0 = o.t0;
   c.t_min = o.t_min;
   c.renormalize_interval = 1000;  // McConfig default (spinmc.hpp:120)
+  c.rho_half = o.rho_half ? 1 : 0;  // device-only option (no reference counterpart)
   c.shard_index = 0;
   c.shard_count = 1;
   return c;
@@ -580,12 +581,13 @@ int main(int argc, char** argv) {
         else if (a == "--baseline") o.baseline = value(i);
         else if (a == "--out") o.out_dir = value(i);
         else if (a == "--kernel-log") o.kernel_log = true;
+        else if (a == "--rho-half") o.rho_half = true;
         else if (a == "--help" || a == "-h") {
           std::printf("taskgemm_b200 run [--spins S] [--steps N] [--procedures P] [--devices G] "
                       "[--mode device] [--entropy renyi-2|von-neumann] [--objective max|min] [--t0 T] "
                       "[--t-min T] [--initial-state product|random] [--seed X] "
                       "[--sweep-procedures a,b,..] [--repeats R] [--baseline report.json] "
-                      "[--out DIR] [--kernel-log]\n");
+                      "[--out DIR] [--kernel-log] [--rho-half]\n");
           return 0;
         } else usage_error("unknown option: " + a);
       }
