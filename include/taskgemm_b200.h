@@ -215,7 +215,8 @@ int tg_hbm_schedule(uint32_t spins, uint64_t rows, int32_t entropy_kind);
  * (13..24) on the queue schedule and writes 16 per-CTA clock64 counters per CTA into
  * stats[ctas * 16] (layout in csrc/hbm_queue.cuh, STATS); *ctas = the grid size (SM count,
  * stats must hold 16 * SM count values). */
-tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* stats, int* ctas);
+tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps, int32_t entropy_kind,
+                               int64_t* stats, int* ctas);
 /* first n xoshiro256++ outputs of derive_stream({seed,p}) computed on the GPU */
 tg_status tg_probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* out_host);
 /* gate stream of `steps` steps (site, U[32], u_accept) generated by the device producer */

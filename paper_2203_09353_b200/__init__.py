@@ -164,7 +164,8 @@ def lib() -> C.CDLL:
     L.tg_probe_entropy_kind.argtypes = [C.c_uint32, C.c_uint64, _dp, C.c_int32, _dp, _dp]
     L.tg_set_perturb_gemm.argtypes = [C.c_int]
     L.tg_hbm_schedule.argtypes = [C.c_uint32, C.c_uint64, C.c_int32]
-    L.tg_probe_queue_stats.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64), C.POINTER(C.c_int)]
+    L.tg_probe_queue_stats.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int32, C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int)]
     L.tg_probe_phase_trace.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(C.c_int64)]
     L.tg_probe_rng_chunking.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int32, C.c_uint64,
                                         C.POINTER(C.c_uint64)]

@@ -508,11 +508,22 @@ namespace {
 constexpr size_t kQueueSlabBudget = size_t{48} << 30;
 constexpr uint64_t kQueueMaxRows = 8192;
 
+// von Neumann above S = 15 exists on the queue schedule only (vn_large.cuh)
+bool vn_large(uint32_t spins, int entropy_kind) {
+  return entropy_kind == TG_VON_NEUMANN && spins >= static_cast<uint32_t>(kVnQueueMinSpins) &&
+         spins <= static_cast<uint32_t>(kVnQueueMaxSpins);
+}
+size_t queue_row_bytes(uint32_t spins, int entropy_kind) {  // slab (+ rho planes)
+  return (size_t{32} << spins) + (vn_large(spins, entropy_kind) ? 8 * hbmq::QLayout::rho_doubles(spins) : 0);
+}
+
 bool queue_possible(uint32_t spins, uint64_t rows, int entropy_kind, bool half = false) {
-  if (entropy_kind != TG_RENYI2 || rows == 0 || rows > kQueueMaxRows || !hbm_use_tma()) return false;
+  if ((entropy_kind != TG_RENYI2 && !vn_large(spins, entropy_kind)) || rows == 0 || rows > kQueueMaxRows ||
+      !hbm_use_tma())
+    return false;
   const char* env = std::getenv("TG_HBM_QUEUE");
-  if (env && env[0] == '0' && !half) return false;
-  return rows * (size_t{32} << spins) <= kQueueSlabBudget;
+  if (env && env[0] == '0' && !half && !vn_large(spins, entropy_kind)) return false;
+  return rows * queue_row_bytes(spins, entropy_kind) <= kQueueSlabBudget;
 }
 
 // Schedule choice by a tile-time model. Cluster schedule: ceil(rows / clusters) waves of
@@ -524,7 +535,7 @@ bool queue_possible(uint32_t spins, uint64_t rows, int entropy_kind, bool half =
 // phase-trace probe force the cluster schedule.
 bool queue_pick(uint32_t spins, uint64_t rows, int entropy_kind, int device, bool trace, bool half = false) {
   if (trace || !queue_possible(spins, rows, entropy_kind, half)) return false;
-  if (half) return true;  // rho_half runs on the queue schedule only
+  if (half || vn_large(spins, entropy_kind)) return true;  // options that run on the queue only
   const char* env = std::getenv("TG_HBM_QUEUE");
   if (env && env[0] == '1') return true;
   if (std::getenv("TG_HBM_CTAS_PER_REPLICA")) return false;
@@ -551,8 +562,8 @@ uint64_t anneal_hbm_queue_rows(uint32_t spins, uint64_t rows, int entropy_kind) 
   return queue_possible(spins, rows, entropy_kind, true) ? rows : 0;
 }
 
-uint64_t anneal_hbm_queue_max_rows(uint32_t spins) {
-  return std::min<uint64_t>(kQueueMaxRows, kQueueSlabBudget / (size_t{32} << spins));
+uint64_t anneal_hbm_queue_max_rows(uint32_t spins, int entropy_kind) {
+  return std::min<uint64_t>(kQueueMaxRows, kQueueSlabBudget / queue_row_bytes(spins, entropy_kind));
 }
 
 int anneal_hbm_schedule(const AnnealParams& p, int device) {
@@ -565,9 +576,11 @@ size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int
   const uint64_t qrows = anneal_hbm_queue_rows(spins, rows, entropy_kind);
   const size_t da = size_t{1} << (spins / 2);
   // von Neumann with d_a > 64: rho (2 planes of d_a^2) after each slab (vn_packed.cuh)
-  const size_t rho = entropy_kind == 0 && da > static_cast<size_t>(hbm::TB) ? 2 * da * da : 0;
+  const bool big_vn = vn_large(spins, entropy_kind);  // queue only: rho lives in the queue region
+  const size_t rho = entropy_kind == 0 && da > static_cast<size_t>(hbm::TB) && !big_vn ? 2 * da * da : 0;
   const size_t slab = (4 * (size_t{1} << spins) + rho) * sizeof(double);
-  return static_cast<size_t>(std::max(clusters, qrows)) * slab + (qrows ? hbmq::QLayout::bytes(spins, qrows) : 0);
+  return static_cast<size_t>(big_vn ? qrows : std::max(clusters, qrows)) * slab +
+         (qrows ? hbmq::QLayout::bytes(spins, qrows, vn_large(spins, entropy_kind)) : 0);
 }
 
 uint64_t anneal_hbm_wave_rows(const AnnealParams& p) {  // co-resident clusters = replicas per wave
@@ -592,7 +605,9 @@ cudaError_t launch_queue(const AnnealParams& p, cudaStream_t stream, int dev, in
                         p.queue_rows);
   e = cudaMemsetAsync(L.ctr, 0, L.counter_bytes, stream);
   if (e != cudaSuccess) return e;
-  auto kern = stats ? hbmq::anneal_queue_kernel<true> : hbmq::anneal_queue_kernel<false>;
+  const bool vn = p.entropy_kind == TG_VON_NEUMANN;
+  auto kern = vn ? (stats ? hbmq::anneal_queue_kernel<true, 1> : hbmq::anneal_queue_kernel<false, 1>)
+                 : (stats ? hbmq::anneal_queue_kernel<true, 0> : hbmq::anneal_queue_kernel<false, 0>);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbmq::kQSmemBytes);
   if (e != cudaSuccess) return e;
   const int grid = sms > 0 ? sms : 1;  // one CTA per SM; the queue is deadlock-free at any residency
@@ -602,8 +617,8 @@ cudaError_t launch_queue(const AnnealParams& p, cudaStream_t stream, int dev, in
                  static_cast<unsigned long long>(p.rows), grid);
   kern<<<grid, hbmq::kQThreads, hbmq::kQSmemBytes, stream>>>(p, tmap);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  return launch_finish_renyi(p, stream);
+  if (e != cudaSuccess || vn) return e;
+  return launch_finish_renyi(p, stream);  // Renyi-2 traces were stored as raw ||rho||_F^2
 }
 
 }  // namespace
@@ -612,7 +627,7 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
                               bool trace) {
   if (p.spins < 13 || p.spins > 24) return cudaErrorInvalidValue;
   if (!p.workspace) return cudaErrorInvalidValue;
-  if (p.entropy_kind == 0 && p.spins > static_cast<uint32_t>(kVnMaxSpins)) return cudaErrorInvalidValue;
+  if (p.entropy_kind == 0 && p.spins > static_cast<uint32_t>(kVnQueueMaxSpins)) return cudaErrorInvalidValue;
   int dev = 0, cs = 1;
   uint64_t clusters = 0;
   cudaGetDevice(&dev);
@@ -624,7 +639,7 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
       (queue_stats ? queue_possible(p.spins, p.rows, p.entropy_kind)
                    : queue_pick(p.spins, p.rows, p.entropy_kind, dev, trace, p.rho_half != 0)))
     return launch_queue(p, stream, dev, grid_out, queue_stats);
-  if (p.rho_half) return cudaErrorInvalidValue;  // the Hermitian half exists on the queue schedule only
+  if (p.rho_half || vn_large(p.spins, p.entropy_kind)) return cudaErrorInvalidValue;  // queue-only options
   cudaError_t e = hbm_geometry(p.spins, p.rows, p.entropy_kind, dev, cs, clusters);
   if (e != cudaSuccess) return e;
   // never more clusters than the workspace has slabs (the persistent loop strides over rows)

@@ -93,9 +93,9 @@ tg_status validate(const tg_anneal_config* c) {
                                " amplitudes per replica)");
   if (c->entropy_kind != TG_RENYI2 && c->entropy_kind != TG_VON_NEUMANN)
     return fail(TG_ECONFIG, "entropy_kind must be von-neumann or renyi-2");
-  if (c->entropy_kind == TG_VON_NEUMANN && c->spins > static_cast<uint32_t>(tg::kVnMaxSpins))
-    return fail(TG_EINVAL, "device von-neumann entropy covers spins <= " + std::to_string(tg::kVnMaxSpins) +
-                               " (rho resident in shared memory); use renyi-2");
+  if (c->entropy_kind == TG_VON_NEUMANN && c->spins > static_cast<uint32_t>(tg::kVnQueueMaxSpins))
+    return fail(TG_EINVAL, "device von-neumann entropy covers spins <= " + std::to_string(tg::kVnQueueMaxSpins) +
+                               " (d_a <= 1024); use renyi-2");
   if (c->inject_fault < 0 || c->inject_fault > 2) return fail(TG_ECONFIG, "inject_fault must be 0, 1 or 2");
   if (c->rho_half != 0 && c->rho_half != 1) return fail(TG_ECONFIG, "rho_half must be 0 or 1");
   if (c->rho_half && (c->entropy_kind != TG_RENYI2 || c->spins <= static_cast<uint32_t>(tg::kSmemMaxSpins)))
@@ -161,7 +161,8 @@ uint64_t slab_clusters(uint32_t spins, uint64_t rows, int device) {
 size_t workspace_for(const tg::AnnealParams& p, int device) {
   const size_t per_row = tg::gate_stream_bytes_per_row(p.spins, p.steps, p.initial_state == 1);
   uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(p.rows, kStreamBudget / per_row));
-  if (p.rho_half) batch = std::max<uint64_t>(1, std::min<uint64_t>(batch, tg::anneal_hbm_queue_max_rows(p.spins)));
+  if (p.rho_half || (p.entropy_kind == TG_VON_NEUMANN && p.spins >= static_cast<uint32_t>(tg::kVnQueueMinSpins)))
+    batch = std::max<uint64_t>(1, std::min<uint64_t>(batch, tg::anneal_hbm_queue_max_rows(p.spins, p.entropy_kind)));
   return batch * per_row + slab_bytes(p.spins, batch, device, p.entropy_kind) + 1024;
 }
 
@@ -177,7 +178,8 @@ cudaError_t launch(const tg::AnnealParams& p, void* ws, size_t ws_bytes, cudaStr
   if (p.rows == 0) return cudaSuccess;
   const size_t per_row = tg::gate_stream_bytes_per_row(p.spins, p.steps, p.initial_state == 1);
   uint64_t batch = std::min<uint64_t>(p.rows, kStreamBudget / per_row);
-  if (p.rho_half) batch = std::min<uint64_t>(batch, tg::anneal_hbm_queue_max_rows(p.spins));  // queue schedule only
+  const bool queue_only = p.rho_half || (p.entropy_kind == TG_VON_NEUMANN && p.spins >= static_cast<uint32_t>(tg::kVnQueueMinSpins));
+  if (queue_only) batch = std::min<uint64_t>(batch, tg::anneal_hbm_queue_max_rows(p.spins, p.entropy_kind));
   while (batch > 0 && batch * per_row + slab_bytes(p.spins, batch, dev, p.entropy_kind) + 1024 > ws_bytes) --batch;
   if (batch == 0) return cudaErrorMemoryAllocation;
   const size_t stream_bytes = batch * per_row;
@@ -895,7 +897,8 @@ tg_status tg_probe_phase_trace(uint32_t spins, uint64_t replicas, uint64_t steps
   return TG_OK;
 }
 
-tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps, int64_t* stats, int* ctas) {
+tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps, int32_t entropy_kind, int64_t* stats,
+                               int* ctas) {
   if (spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) || spins > 24) return fail(TG_EINVAL, "queue stats cover spins in [13,24]");
   if (!stats || !ctas) return fail(TG_EINVAL, "stats / ctas must not be NULL");
   setenv("TG_HBM_QUEUE", "1", 1);
@@ -904,7 +907,7 @@ tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps
   c.devices = 1;
   c.steps = steps;
   c.procedures = replicas;
-  c.entropy_kind = TG_RENYI2;
+  c.entropy_kind = entropy_kind;
   c.t0 = 1.0;
   c.t_min = 1e-3;
   c.renormalize_interval = 1000;

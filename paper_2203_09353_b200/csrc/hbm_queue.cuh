@@ -34,6 +34,7 @@
 #pragma once
 #include "hbm_tier.cuh"
 #include "tg_internal.h"
+#include "vn_large.cuh"
 
 namespace tg {
 namespace hbmq {
@@ -63,6 +64,7 @@ struct QMeta {  // one pipeline stage entry (written by the producer)
 
 struct QHeader {
   HHeader h;
+  uint64_t ctl_done;  // von Neumann: a DEC item has released the stage buffers (its scratch)
   QMeta meta[kStages];
   QRow row;          // row-state snapshot for a control item
   int64_t stat[16];  // STATS probe only (anneal_queue_kernel<true>)
@@ -85,23 +87,28 @@ struct QGeo {
     const uint64_t p = groups / 4096;
     return static_cast<uint32_t>(p < 1 ? 1 : (p > 16 ? 16 : p));
   }
-  __host__ __device__ QGeo(uint32_t s, uint64_t r, uint64_t st, bool random, uint32_t grid, bool h = false) {
+  bool long_dec;  // von Neumann: the DEC item (an eigen-solve) applies the whole next gate itself
+  __host__ __device__ QGeo(uint32_t s, uint64_t r, uint64_t st, bool random, uint32_t grid, bool h = false,
+                           bool ldec = false) {
     spins = s;
     n = uint64_t{1} << s;
     nt = (1u << (s / 2)) / TB;
     nfull = nt * nt;
     half = h;
+    long_dec = ldec;
     ntt = half ? nt * (nt + 1) / 2 : nfull;
     P = gate_parts(s);
     Ip = P + (random ? 1 : 0);
     rows = r;
     steps = st;
-    BS = ntt + P;  // tiles, DEC (+ gate part 0 of the next step), gate parts 1 .. P-1
+    // tiles, DEC (+ gate part 0 of the next step, or all of it), gate parts 1 .. P-1
+    BS = ntt + (long_dec ? 1 : P);
     const uint64_t want = (2ull * grid + ntt - 1) / ntt;
     const uint64_t lmax = r > 0 ? r - 1 : 0;
     const uint64_t wantG = want + (P > 1 ? (grid + BS - 1) / BS : 0);  // ~ one CTA round after the DEC
     lagG = static_cast<uint32_t>(wantG < lmax ? wantG : lmax);
     lagD = static_cast<uint32_t>(want < lagG ? want : lagG);
+    if (long_dec) lagG = lagD = 0;  // a DEC outlasts many CTA rounds of tiles: pull it right after its tiles
     pro = r * Ip;
     K = (st + 1) * r;
     total = pro + (K + lagG) * BS;
@@ -172,11 +179,13 @@ struct QLayout {
   unsigned long long* tiles_done;
   unsigned long long* dec_done;
   size_t counter_bytes;
+  double* rho;       // von Neumann: [cap][2][d_a^2] planes Re, Im of rho (column-major)
   __host__ __device__ static size_t align(size_t b) { return (b + 255) / 256 * 256; }
-  __host__ __device__ static size_t bytes(uint32_t spins, uint64_t cap) {
+  __host__ __device__ static size_t rho_doubles(uint32_t spins) { return 2 * (size_t{1} << (2 * (spins / 2))); }
+  __host__ __device__ static size_t bytes(uint32_t spins, uint64_t cap, bool vn = false) {
     const uint64_t nt = (uint64_t{1} << (spins / 2)) / TB;
     return align(cap * nt * nt * kThreads * 8) + align(cap * nt * 2 * kThreads * 8) + align(cap * sizeof(QRow)) +
-           align((16 + 3 * cap) * 8);
+           align((16 + 3 * cap) * 8) + (vn ? align(cap * rho_doubles(spins) * 8) : 0);
   }
   __host__ __device__ QLayout(char* base, uint32_t spins, uint64_t cap) {
     const uint64_t nt = (uint64_t{1} << (spins / 2)) / TB;
@@ -191,6 +200,8 @@ struct QLayout {
     tiles_done = gate_done + cap;
     dec_done = tiles_done + cap;
     counter_bytes = align((16 + 3 * cap) * 8);
+    base += counter_bytes;
+    rho = reinterpret_cast<double*>(base);
   }
 };
 
@@ -289,7 +300,9 @@ __device__ void q_renormalize(const Geo& G, double* X, double* Y, int tid, int w
 //  4 producer waits for free stages, 5 producer dependency waits (tiles), 6 control items,
 //  7 their dependency waits, 8 tiles, 9 DEC, 10 GATE, 11 INIT + NORM items, 12 DEC clocks,
 //  13 GATE clocks, 14 producer queue pulls (atomics incl. empty slots)
-template <bool STATS = false>
+// KIND 0: Renyi-2 (||rho||_F^2 partials); KIND 1: von Neumann for 16 <= S <= 21 (vn_large.cuh):
+// TILE items store rho to the row's planes, the DEC item diagonalises it.
+template <bool STATS = false, int KIND = 0>
 __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const AnnealParams P,
                                                                     const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -298,7 +311,7 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
   const uint32_t sbase = smem_u32(smem_raw);
   double* stages = reinterpret_cast<double*>(smem_raw + (((sbase + kQHeaderBytes + 1023u) & ~1023u) - sbase));
   const Geo G(static_cast<int>(P.spins));
-  const QGeo q(P.spins, P.rows, P.steps, P.initial_state == 1, gridDim.x, P.rho_half != 0);
+  const QGeo q(P.spins, P.rows, P.steps, P.initial_state == 1, gridDim.x, P.rho_half != 0, KIND == 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt = G.tiles(), nk = G.kchunks(), lnt = G.la - 6;
   const uint64_t cap = P.queue_rows;
@@ -313,17 +326,20 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
       mbar_init(&H.full[s], 1);
       mbar_init(&H.empty[s], kWarps);
     }
+    mbar_init(&Q.ctl_done, 1);
     fence_mbar_init();
     if (STATS)
       for (int i = 0; i < 16; ++i) Q.stat[i] = 0;
   }
   __syncthreads();  // the last CTA-wide barrier: from here on consumers use csync()
+  static_assert(KIND == 0 || sizeof(vnl::Scratch) <= kStages * kStage * 8, "vN scratch fits the stages");
 
   // ================================================================== producer (1 thread)
   if (tid >= kThreads) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
     if (tid != kThreads) return;
     uint64_t issued = 0;
+    uint32_t ctl_par = 0;
     auto stage_for = [&](uint64_t e) {  // wait until entry e's stage is free
       const int s = static_cast<int>(e % kStages);
       if (e >= static_cast<uint64_t>(kStages)) {
@@ -346,6 +362,10 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
         Q.meta[s].x = x;
         mbar_arrive(&H.full[s]);
         if (x.type == kItemEnd) break;
+        if (KIND == 1 && x.type == kItemDec) {  // its eigen-solver uses the stage buffers as scratch
+          mbar_wait(&Q.ctl_done, ctl_par);
+          ctl_par ^= 1;
+        }
         continue;
       }
       // TILE(r, s, t): wait for its gate (or initial state), then its row's buffer
@@ -474,14 +494,14 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     const bool next_gate = static_cast<uint64_t>(s + 1) < P.steps;
     if (Q.row.err) {
       sync_signal(&L.dec_done[r]);
-      if (next_gate && tid == 0) signal(&L.gate_done[r], 1);  // part 0 (no work)
+      if (next_gate && tid == 0) signal(&L.gate_done[r], q.long_dec ? q.P : 1);  // its gate parts (no work)
       return;
     }
     // replay the per-thread chains of rho_partials_tma (CS = 1, tiles in ascending order)
     double rho[kChains] = {0.0, 0.0, 0.0, 0.0}, tr[kChains] = {0.0, 0.0, 0.0, 0.0};
     {
       const double* tvr = L.tv + r * q.nfull * kThreads + tid;
-      for (uint32_t t0 = 0; t0 < q.nfull; t0 += kChains) {
+      for (uint32_t t0 = 0; KIND == 0 && t0 < q.nfull; t0 += kChains) {
 #pragma unroll
         for (int c = 0; c < kChains; ++c) {
           const uint32_t t = t0 + c;  // rho_half: lower tiles (ti > tj) were not formed
@@ -513,6 +533,12 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     q_publish(H, tid);
     double rho2, trv;
     totals<1>(H, rho2, trv);
+    if constexpr (KIND == 1) {  // von Neumann: eigenvalues of this step's rho (stages = scratch)
+      const size_t da = size_t{1} << G.la;
+      double* Rr = L.rho + r * QLayout::rho_doubles(P.spins);
+      rho2 = vnl::entropy(Rr, Rr + da * da, static_cast<int>(da), *reinterpret_cast<vnl::Scratch*>(stages), tid,
+                          [] { csync(); });  // thread 0: the entropy (the trace value of this proposal)
+    }
     if (tid == 0) {
       QRow w = Q.row;
       const bool bad = smem::not_normalized(trv);
@@ -538,7 +564,9 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
           P.status_step[r] = s;
           if (P.status_norm) P.status_norm[r] = __dsqrt_rn(trv);
         } else {
-          const smem::Verdict v = smem::decide_audit(rho2, w.cur_e, g, P.objective, P.tie_eps);
+          // KIND 0: the lean decision on ||rho||^2; KIND 1: spinmc.cpp:203-207 on the entropies
+          const smem::Verdict v = KIND == 0 ? smem::decide_audit(rho2, w.cur_e, g, P.objective, P.tie_eps)
+                                            : smem::decide_reference(rho2, w.cur_e, g, P.objective, P.tie_eps);
           acc = v.acc;
           smem::audit(P, r, static_cast<uint64_t>(s), g, v);
           if (acc) {
@@ -565,9 +593,12 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     if (s >= 0 && !Q.row.err && P.renorm > 0 && (static_cast<uint64_t>(s) + 1) % P.renorm == 0)
       q_renormalize(G, PX(r, Q.row.cur), PY(r, Q.row.cur), tid, warp, lane, H);  // spinmc.cpp:246-248
     sync_signal(&L.dec_done[r]);
-    if (next_gate) {  // part 0 of the next step's gate, on the state just decided
-      if (!Q.row.err) gate_part(r, s + 1, 0, Q.row.cur);
-      sync_signal(&L.gate_done[r]);
+    if (next_gate) {  // part 0 (von Neumann: every part) of the next step's gate, on the state just decided
+      const int parts = q.long_dec ? static_cast<int>(q.P) : 1;
+      if (!Q.row.err)
+        for (int part = 0; part < parts; ++part) gate_part(r, s + 1, part, Q.row.cur);
+      csync();
+      if (tid == 0) signal(&L.gate_done[r], static_cast<unsigned long long>(parts));
     }
   };
 
@@ -599,6 +630,7 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
       const int64_t a = clk();
       run_control(md.x);
       csync();
+      if (KIND == 1 && md.x.type == kItemDec && tid == 0) mbar_arrive(&Q.ctl_done);  // scratch released
       if (STATS && tid == 0) {
         const int64_t d = clk() - a;
         stat_add(6, d);
@@ -678,10 +710,26 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
       const double x0 = __ldcg(PX(r, md.buf)), y0 = __ldcg(PY(r, md.buf));
       fault_term(cr[0][0][0], x0, y0);
     }
-    double rho1[kChains] = {0.0, 0.0, 0.0, 0.0};
-    tile_fold(cr, ci, rho1, 0, false);  // rho1[0] = 0.0 + tv (tile_fold's arithmetic)
-    if (q.half && !diag) rho1[0] += rho1[0];  // rho_half: the mirrored lower tile (exact)
-    __stcg(L.tv + (r * q.nfull + static_cast<uint64_t>(md.t)) * kThreads + tid, rho1[0]);
+    if constexpr (KIND == 1) {  // rho itself, for the DEC item's eigen-solver
+      const size_t da = size_t{1} << G.la;
+      double* Rr = L.rho + r * QLayout::rho_doubles(P.spins);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const size_t o = static_cast<size_t>(ti * TB + (wr * 2 + i) * 8 + m) +
+                             static_cast<size_t>(tj * TB + (wc * 4 + j) * 8 + 2 * kq + e) * da;
+            __stcg(Rr + o, cr[i][j][e]);
+            __stcg(Rr + da * da + o, ci[i][j][e]);
+          }
+    } else {
+      double rho1[kChains] = {0.0, 0.0, 0.0, 0.0};
+      tile_fold(cr, ci, rho1, 0, false);  // rho1[0] = 0.0 + tv (tile_fold's arithmetic)
+      if (q.half && !diag) rho1[0] += rho1[0];  // rho_half: the mirrored lower tile (exact)
+      __stcg(L.tv + (r * q.nfull + static_cast<uint64_t>(md.t)) * kThreads + tid, rho1[0]);
+    }
     __syncwarp();
     if (lane == 0) signal(&L.tiles_done[r], 1);
     if (STATS && tid == 32) {

@@ -69,7 +69,8 @@ enum : int32_t { kRowOk = 0, kRowNotNormalized = 2 };
 
 constexpr int kSmemMaxSpins = 12;
 constexpr uint64_t kMaxSteps = uint64_t{1} << 22;  // gate_stream.cu jump tables (kJumpBits)
-constexpr int kVnMaxSpins = 15;  // device von Neumann: d_a <= 64 (vn.cuh: SMEM tier, HBM tier S=13), d_a = 128 (vn_packed.cuh: S=14,15)
+constexpr int kVnMaxSpins = 15;
+constexpr int kVnQueueMinSpins = 16, kVnQueueMaxSpins = 21;  // von Neumann on the work queue (vn_large.cuh: d_a 256..1024)  // device von Neumann: d_a <= 64 (vn.cuh: SMEM tier, HBM tier S=13), d_a = 128 (vn_packed.cuh: S=14,15)
 
 // anneal_smem.cu (S <= 12)
 // replicas processed per wave by one launch (resident CTAs / clusters), 0 if unknown
@@ -86,7 +87,7 @@ size_t anneal_hbm_workspace_bytes(uint32_t spins, uint64_t rows, int device, int
 int anneal_hbm_schedule(const AnnealParams& p, int device);
 uint64_t anneal_hbm_slab_clusters(uint64_t rows, int device);  // slabs for launches of <= rows replicas
 uint64_t anneal_hbm_queue_rows(uint32_t spins, uint64_t rows, int entropy_kind);  // queue region capacity
-uint64_t anneal_hbm_queue_max_rows(uint32_t spins);  // largest launch the queue schedule takes
+uint64_t anneal_hbm_queue_max_rows(uint32_t spins, int entropy_kind);  // largest launch the queue schedule takes
 
 // probes.cu
 cudaError_t probe_rng(uint64_t seed, uint64_t p, uint64_t n, uint64_t* d_out, cudaStream_t s);

@@ -49,7 +49,7 @@ def test_version():
     (dict(t0=1e-3, t_min=1.0), tg.ConfigError, "anneal schedule requires 0 < t_min <= t0"),
     (dict(t_min=0.0), tg.ConfigError, "anneal schedule requires 0 < t_min <= t0"),
     (dict(spins=26), ValueError, "device tiers cover spins <= 24"),
-    (dict(entropy_kind="von-neumann", spins=16), ValueError, "device von-neumann entropy covers spins <= 15"),
+    (dict(entropy_kind="von-neumann", spins=22), ValueError, "device von-neumann entropy covers spins <= 21"),
     (dict(entropy_kind="tsallis"), tg.ConfigError, "unknown entropy_kind"),
     (dict(shard_index=2, shard_count=2), tg.ConfigError, "shard_index"),
 ])

@@ -106,8 +106,8 @@ def test_run_von_neumann_config1(tmp_path):
     rep = json.loads((tmp_path / "report.json").read_text())
     assert rep["config"]["entropy"] == "von-neumann"
     assert abs(rep["average_entropy_nats"] - 2.360208109374111) <= 1e-10 * 2.37
-    code, out = run(["run", "--spins", "16", "--steps", "1", "--entropy", "von-neumann", "--out", str(tmp_path / "x")])
-    assert code != 0 and "device von-neumann entropy covers spins <= 15" in out
+    code, out = run(["run", "--spins", "22", "--steps", "1", "--entropy", "von-neumann", "--out", str(tmp_path / "x")])
+    assert code != 0 and "device von-neumann entropy covers spins <= 21" in out
 
 
 @gpu

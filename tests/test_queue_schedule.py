@@ -178,3 +178,39 @@ def test_rho_half_renormalisation_and_errors(device, monkeypatch):
                               fault_step=2, rho_half=True)
     with pytest.raises(ValueError, match="entanglement_entropy: state not normalized"):
         device.run(bad)
+
+
+# --------------------------------- von Neumann above S = 15 (vn_large.cuh, work queue only)
+@pytest.mark.parametrize("spins,procs,steps,obj", [(16, 2, 3, "max"), (17, 1, 2, "min")])
+def test_von_neumann_large_vs_oracle(device, oracle, spins, procs, steps, obj):
+    """d_a = 256: TILE items store rho, the DEC item tridiagonalises it in global memory
+    (Householder, one fused update + matvec pass per reflector) and bisects the Sturm counts;
+    the oracle diagonalises with the reference's cyclic Jacobi. Sites and accept flags
+    bit-exact, entropies within 1e-10."""
+    cfg = tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=19, entropy_kind="von-neumann",
+                              objective=obj, initial_state="random")
+    rep = device.run(cfg)
+    again = device.run(cfg)
+    assert_bitwise(rep, again)
+    want = oracle.run(McCfg(spins=spins, steps=steps, seed=19, entropy_kind=0, objective=1 if obj == "min" else 0,
+                            initial_state=1), 0, procs, threads=procs)
+    assert np.array_equal(rep.sites, want.sites)
+    assert np.array_equal(rep.accepted, want.accepted)
+    assert close(rep.initial_entropy, want.initial).all(), np.abs(rep.initial_entropy - want.initial).max()
+    assert close(rep.entropies, want.entropies).all(), np.abs(rep.entropies - want.entropies).max()
+
+
+@pytest.mark.parametrize("spins", [18, 20])
+def test_von_neumann_large_invariants(device, spins):
+    """d_a = 512 and 1024 (config 4's chain), beyond the oracle's reach: a Haar-random start's
+    von Neumann entropy is at least its Renyi-2 entropy (same state, same seed) and below
+    floor(S/2) ln 2; traces stay in that range; reruns bitwise."""
+    import math
+    base = dict(spins=spins, steps=2, procedures=2, seed=23, initial_state="random")
+    vn = device.run(tg.ExperimentConfig(entropy_kind="von-neumann", **base))
+    r2 = device.run(tg.ExperimentConfig(entropy_kind="renyi-2", **base))
+    assert_bitwise(vn, device.run(tg.ExperimentConfig(entropy_kind="von-neumann", **base)))
+    bound = (spins // 2) * math.log(2) + 1e-9
+    assert np.all(vn.initial_entropy >= r2.initial_entropy - 1e-12)
+    assert np.all(vn.initial_entropy <= bound) and np.all(vn.entropies <= bound) and np.all(vn.entropies >= 0)
+    assert np.array_equal(vn.sites, r2.sites)  # the proposal stream does not depend on the entropy

@@ -1,0 +1,4 @@
+timeout 600 python tools/queue_stats.py 16 148 3 von-neumann | head -16
+timeout 1200 python -m pytest tests/test_queue_schedule.py -x -q 2>&1 | tail -2
+timeout 900 python bench.py --config 3 --entropy von-neumann --replicas 512 --mc-steps 5 --steps 1 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c3 vN 512x5', d['value'], d['roofline']['kernel'])"
+timeout 900 python bench.py --entropy von-neumann --replicas 148 --mc-steps 2 --steps 1 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c4 vN 148x2', d['value'], d['roofline']['kernel'])"

@@ -1,6 +1,6 @@
 """Per-CTA clock breakdown of the HBM tier's work-queue schedule (tg_probe_queue_stats).
 
-    python tools/queue_stats.py SPINS REPLICAS STEPS
+    python tools/queue_stats.py SPINS REPLICAS STEPS [renyi-2|von-neumann]
 """
 import ctypes as C
 import os
@@ -12,10 +12,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2203_09353_b200 as tg  # noqa: E402
 
 spins, reps, steps = (int(a) for a in sys.argv[1:4])
+kind = 0 if len(sys.argv) > 4 and sys.argv[4] == "von-neumann" else 1
 L = tg.lib()
 buf = (C.c_int64 * (16 * 1024))()
 ctas = C.c_int(0)
-tg._check(L.tg_probe_queue_stats(spins, reps, steps, buf, C.byref(ctas)))
+tg._check(L.tg_probe_queue_stats(spins, reps, steps, kind, buf, C.byref(ctas)))
 s = np.frombuffer(buf, dtype=np.int64)[: 16 * ctas.value].reshape(ctas.value, 16).astype(np.float64)
 names = ["total", "w1 wait stage", "w1 chunk compute", "w1 tile epilogue", "t0 wait stage (+issue)",
          "t0 top issue", "control items", "  dependency waits", "tiles", "DEC", "GATE", "INIT+NORM",
