@@ -67,6 +67,7 @@ struct QHeader {
   uint64_t ctl_done;  // von Neumann: a DEC item has released the stage buffers (its scratch)
   QMeta meta[kStages];
   QRow row;          // row-state snapshot for a control item
+  alignas(16) GateRec rec[2];  // control items: proposal records of steps s (decision) and s + 1 (gate)
   int64_t stat[16];  // STATS probe only (anneal_queue_kernel<true>)
 };
 constexpr int kQHeaderBytes = (static_cast<int>(sizeof(QHeader)) + 127) / 128 * 128;
@@ -299,7 +300,7 @@ __device__ void q_renormalize(const Geo& G, double* X, double* Y, int tid, int w
 //  0 total, 1 warp-1 waits for stage data, 2 warp-1 chunk compute, 3 warp-1 tile epilogues,
 //  4 producer waits for free stages, 5 producer dependency waits (tiles), 6 control items,
 //  7 their dependency waits, 8 tiles, 9 DEC, 10 GATE, 11 INIT + NORM items, 12 DEC clocks,
-//  13 GATE clocks, 14 producer queue pulls (atomics incl. empty slots)
+//  13 GATE clocks, 14 producer queue pulls (atomics incl. empty slots), 15 gate passes inside DEC items
 // KIND 0: Renyi-2 (||rho||_F^2 partials); KIND 1: von Neumann for 16 <= S <= 21 (vn_large.cuh):
 // TILE items store rho to the row's planes, the DEC item diagonalises it.
 template <bool STATS = false, int KIND = 0>
@@ -436,10 +437,25 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     csync();
     if (tid == 0) signal(c, 1);
   };
-  auto gate_part = [&](uint64_t r, int64_t s, int part, int cur) {  // spinmc.cpp:91-136 on 1/P of the groups
-    const GateRec& g = P.gates[static_cast<uint64_t>(s) * P.rows + r];
+  // A control item's proposal records (steps s0 and s0 + 1 of row r, when they exist) are
+  // copied to SMEM by cp.async as the item starts, so the global round trips overlap its
+  // dependency wait and fold instead of sitting on the decision / gate path; rec_wait()
+  // (every consumer thread) completes them before the next barrier.
+  auto rec_fetch = [&](uint64_t r, int64_t s0) {
+    if (tid < 36) {
+      const int64_t s = s0 + tid / 18;
+      if (s >= 0 && static_cast<uint64_t>(s) < P.steps)
+        cp_async16(reinterpret_cast<char*>(&Q.rec[tid / 18]) + 16 * (tid % 18),
+                   reinterpret_cast<const char*>(P.gates + static_cast<uint64_t>(s) * P.rows + r) + 16 * (tid % 18));
+      cp_async_commit();
+    }
+  };
+  auto rec_wait = [&]() {
+    if (tid < 36) cp_async_wait<0>();
+  };
+  auto gate_part = [&](uint64_t r, const GateRec& g, int part, int cur) {  // spinmc.cpp:91-136 on 1/P of the groups
     const int groups = G.n / 4, per = groups / static_cast<int>(q.P), g0 = part * per;
-    gate_pass(PX(r, cur), PY(r, cur), PX(r, cur ^ 1), PY(r, cur ^ 1), __ldg(&g.site), g, g0, g0 + per, tid, kThreads);
+    gate_pass(PX(r, cur), PY(r, cur), PX(r, cur ^ 1), PY(r, cur ^ 1), g.site, g, g0, g0 + per, tid, kThreads);
     fence_proxy_async_global();  // psi' is read by the TMA engine
   };
   auto run_control = [&](const Item& x) {
@@ -475,21 +491,25 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
       return;
     }
     if (x.type == kItemGate) {
+      rec_fetch(r, x.s - 1);  // rec[1] = step x.s
       if (tid == 0) {
         wait_dep(&L.dec_done[r], static_cast<unsigned long long>(x.s + 1));
         Q.row = load_row(&L.row[r]);
       }
+      rec_wait();
       csync();
-      if (!Q.row.err) gate_part(r, x.s, x.part, Q.row.cur);
+      if (!Q.row.err) gate_part(r, Q.rec[1], x.part, Q.row.cur);
       sync_signal(&L.gate_done[r]);
       return;
     }
     // DEC(r, s)
     const int64_t s = x.s;
+    rec_fetch(r, s);  // rec[0] = step s (the decision), rec[1] = step s + 1 (the next gate)
     if (tid == 0) {
       wait_dep(&L.tiles_done[r], q.tiles_target(s));
       Q.row = load_row(&L.row[r]);
     }
+    rec_wait();
     csync();
     const bool next_gate = static_cast<uint64_t>(s + 1) < P.steps;
     if (Q.row.err) {
@@ -558,7 +578,7 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
           w.t_prev = now;
         }
       } else {
-        const GateRec& g = P.gates[static_cast<uint64_t>(s) * P.rows + r];
+        const GateRec& g = Q.rec[0];
         if (bad) {
           P.status[r] = kRowNotNormalized;
           P.status_step[r] = s;
@@ -592,11 +612,15 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     csync();
     if (s >= 0 && !Q.row.err && P.renorm > 0 && (static_cast<uint64_t>(s) + 1) % P.renorm == 0)
       q_renormalize(G, PX(r, Q.row.cur), PY(r, Q.row.cur), tid, warp, lane, H);  // spinmc.cpp:246-248
-    sync_signal(&L.dec_done[r]);
+    // dec_done is waited on by GATE items only: none exist when the DEC applies the whole gate
+    const bool gate_items = !q.long_dec && q.P > 1;
+    if (gate_items) sync_signal(&L.dec_done[r]);
     if (next_gate) {  // part 0 (von Neumann: every part) of the next step's gate, on the state just decided
       const int parts = q.long_dec ? static_cast<int>(q.P) : 1;
+      const int64_t g0 = clk();
       if (!Q.row.err)
-        for (int part = 0; part < parts; ++part) gate_part(r, s + 1, part, Q.row.cur);
+        for (int part = 0; part < parts; ++part) gate_part(r, Q.rec[1], part, Q.row.cur);
+      if (STATS && tid == 0) stat_add(15, clk() - g0);
       csync();
       if (tid == 0) signal(&L.gate_done[r], static_cast<unsigned long long>(parts));
     }

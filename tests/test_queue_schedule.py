@@ -43,6 +43,8 @@ CASES = [  # spins, procedures, steps, initial state, objective, renormalize_int
     (16, 3, 6, "random", "max", 1000),    # 16 tiles, 4 gate parts per replica
     (14, 37, 8, "product", "max", 1000),  # more replicas than tiles in flight
     (18, 2, 3, "random", "max", 2),       # 16 gate parts, 64 tiles
+    (14, 200, 6, "product", "max", 4),    # L2 groups of 128 + 72 replicas (QGeo::G)
+    (16, 40, 4, "random", "min", 1000),   # L2 groups of 32 + 8 replicas
 ]
 
 

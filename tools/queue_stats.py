@@ -20,12 +20,12 @@ tg._check(L.tg_probe_queue_stats(spins, reps, steps, kind, buf, C.byref(ctas)))
 s = np.frombuffer(buf, dtype=np.int64)[: 16 * ctas.value].reshape(ctas.value, 16).astype(np.float64)
 names = ["total", "w1 wait stage", "w1 chunk compute", "w1 tile epilogue", "t0 wait stage (+issue)",
          "t0 top issue", "control items", "  dependency waits", "tiles", "DEC", "GATE", "INIT+NORM",
-         "DEC clk", "GATE clk", "no-lead issues", "-"]
+         "DEC clk", "GATE clk", "producer pulls clk", "  gate pass in DEC"]
 tot = s[:, 0].mean()
 print(f"S={spins} replicas={reps} steps={steps} ctas={ctas.value}: {tot:.4g} clk per CTA")
-for i, n in enumerate(names[:15]):
+for i, n in enumerate(names[:16]):
     v = s[:, i]
-    share = f"{100 * v.mean() / tot:6.2f} %" if i in (1, 2, 3, 4, 5, 6, 7, 12, 13) else ""
+    share = f"{100 * v.mean() / tot:6.2f} %" if i in (1, 2, 3, 4, 5, 6, 7, 12, 13, 15) else ""
     print(f"  {n:24s} mean {v.mean():12.4g}  min {v.min():12.4g}  max {v.max():12.4g}  {share}")
 nt = s[:, 8].sum()
 if nt:
