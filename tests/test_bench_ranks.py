@@ -14,12 +14,12 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _bench(tmp_path, gpus, tag, extra=()):
+def _bench(tmp_path, gpus, tag, extra=(), config=2, replicas=37, mc_steps=40):
     out = tmp_path / f"finals_{tag}.npy"
     env = dict(os.environ, TG_BENCH_BACKEND="gloo")
-    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus), "--config", "2", "--scaling",
-           "strong", "--replicas", "37", "--mc-steps", "40", "--steps", "1", "--warmup", "3", "--no-cpu-baseline",
-           "--dump-finals", str(out), *extra]
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus), "--config", str(config), "--scaling",
+           "strong", "--replicas", str(replicas), "--mc-steps", str(mc_steps), "--steps", "1", "--warmup", "3",
+           "--no-cpu-baseline", "--dump-finals", str(out), *extra]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -69,3 +69,15 @@ def test_bench_cpu_sample_extrapolation(reflib):
     assert cb["kind"] == "reference" and cb["cores"] == 2 and cb["value"] > 0
     assert "extrapolated linearly" in cb["sample"]
     assert wall < 30
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_config4_queue(tmp_path):
+    """Config 4's chain (L = 20) split over 2 ranks: each rank runs its replicas p = r (mod 2)
+    on the HBM tier's work queue (the schedule config 4 uses at every rank count); the
+    gathered finals equal the one-rank run's bit for bit."""
+    one, f1 = _bench(tmp_path, 1, "one4", config=4, replicas=6, mc_steps=2)
+    two, f2 = _bench(tmp_path, 2, "two4", config=4, replicas=6, mc_steps=2)
+    assert one["roofline"]["kernel"] == two["roofline"]["kernel"] == "anneal_queue_kernel"
+    assert np.array_equal(f1.view(np.uint64), f2.view(np.uint64))
+    assert one["average_entropy"] == two["average_entropy"]
