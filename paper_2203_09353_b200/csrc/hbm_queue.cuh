@@ -57,7 +57,7 @@ struct QRow {
   int64_t t_prev, t_row0;
 };
 
-struct QMeta {  // one pipeline stage entry (written by the producer)
+struct alignas(8) QMeta {  // one pipeline stage entry (written by the producer, st.async)
   int32_t kind, t, kc, buf;
   Item x;  // TILE: x.r is the row; CONTROL: the item itself
 };
@@ -233,6 +233,29 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Stage metadata is written by the producer with st.async, completing as transaction bytes
+// on the stage's full barrier like the TMA data: the consumers' wait on that barrier orders
+// it (and compute-sanitizer's racecheck, which does not model generic writes released by an
+// mbarrier arrive, sees async-proxy writes only).
+static_assert(sizeof(QMeta) == 40, "QMeta: five 8-byte words");
+__device__ __forceinline__ void st_async_b64(void* dst, uint64_t v, uint64_t* bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(smem_u32(dst)),
+               "l"(v), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void put_meta(QMeta* dst, int32_t kind, int32_t t, int32_t kc, int32_t buf, const Item& x,
+                                         uint64_t* bar) {
+  auto pack = [](int32_t lo, int32_t hi) {
+    return static_cast<uint64_t>(static_cast<uint32_t>(lo)) | (static_cast<uint64_t>(static_cast<uint32_t>(hi)) << 32);
+  };
+  char* d = reinterpret_cast<char*>(dst);
+  st_async_b64(d + 0, pack(kind, t), bar);
+  st_async_b64(d + 8, pack(kc, buf), bar);
+  st_async_b64(d + 16, pack(x.type, x.part), bar);
+  st_async_b64(d + 24, static_cast<uint64_t>(x.s), bar);
+  st_async_b64(d + 32, x.r, bar);
+}
+
 __device__ __forceinline__ QRow load_row(const QRow* p) {
   QRow w;
   w.cur = __ldcg(&p->cur);
@@ -359,9 +382,8 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
       stat_add(14, clk() - a);
       if (x.type != kItemTile) {  // control entry (consumers execute it, in queue order)
         const int s = stage_for(issued++);
-        Q.meta[s].kind = kMetaControl;
-        Q.meta[s].x = x;
-        mbar_arrive(&H.full[s]);
+        mbar_expect_tx(&H.full[s], sizeof(QMeta));
+        put_meta(&Q.meta[s], kMetaControl, 0, 0, 0, x, &H.full[s]);
         if (x.type == kItemEnd) break;
         if (KIND == 1 && x.type == kItemDec) {  // its eigen-solver uses the stage buffers as scratch
           mbar_wait(&Q.ctl_done, ctl_par);
@@ -386,14 +408,9 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
       const bool diag = ti == tj;
       for (int kc = 0; kc < nk; ++kc) {
         const int s = stage_for(issued++);
-        QMeta& md = Q.meta[s];
-        md.kind = kMetaTile;
-        md.t = t;
-        md.kc = kc;
-        md.buf = buf;
-        md.x = x;
         double* st = stages + s * kStage;
-        mbar_expect_tx(&H.full[s], diag ? kTmaStageBytes / 2 : kTmaStageBytes);
+        mbar_expect_tx(&H.full[s], (diag ? kTmaStageBytes / 2 : kTmaStageBytes) + sizeof(QMeta));
+        put_meta(&Q.meta[s], kMetaTile, t, kc, buf, x, &H.full[s]);
         for (int h = 0; h < 2; ++h) {
           tma_load_5d(st + h * kTmaBox, &tmap, 0, ti * 4 + 2 * h, kc * KC, 2 * buf, static_cast<int>(x.r), &H.full[s]);
           if (!diag)
