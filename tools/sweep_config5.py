@@ -7,7 +7,7 @@ Every arm reports annealing replica-steps/s for the whole batch, end to end from
 run would take minutes run a replica sample and are scaled linearly in replicas (replicas
 are independent and the scheme is saturated well before the sample size); each row says
 which replicas/steps were actually run. Writes one JSON document (default
-profiles/r01_config5_sweep.json).
+profiles/r02_config5_sweep.json; round 1: r01_config5_sweep.json).
 
   python tools/sweep_config5.py [--out FILE] [--max-replicas N] [--steps 100]
 """
@@ -75,7 +75,7 @@ def cpu_arm(replicas, steps, cores, target_s):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_config5_sweep.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_config5_sweep.json"))
     ap.add_argument("--max-replicas", type=int, default=65536)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--tasked-cap", type=int, default=2048)
@@ -87,7 +87,7 @@ def main():
     from comparators import Comparators
     cmp = Comparators()
     cores = os.cpu_count() or 1
-    sizes = [r for r in (1, 4, 16, 64, 256, 1024, 4096, 16384, 65536) if r <= a.max_replicas]
+    sizes = [r for r in (1, 4, 16, 64, 148, 256, 512, 1024, 4096, 16384, 65536) if r <= a.max_replicas]
     dev = tg.Device([0])
     device_arm(dev, 16, 10)  # warm-up: context, module load, workspace
     cmp.tasked(SPINS, 5, 2, ranks=2)
@@ -96,6 +96,7 @@ def main():
     for r in sizes:
         row = {"replicas": r, "spins": SPINS, "steps": a.steps}
         row["device"], rep = device_arm(dev, r, a.steps)
+        row["device"]["schedule"] = ["cluster", "work queue"][int(tg.lib().tg_hbm_schedule(SPINS, r, 1))]
         row["tasked"], tk = comparator_arm(cmp.tasked, r, a.steps, a.tasked_cap, ranks=a.ranks)
         row["batched"], bt = comparator_arm(cmp.batched, r, a.steps, a.batched_cap)
         # the arms computed the same trajectories (first replicas): flags bit-exact
