@@ -43,8 +43,9 @@ CASES = [  # spins, procedures, steps, initial state, objective, renormalize_int
     (16, 3, 6, "random", "max", 1000),    # 16 tiles, 4 gate parts per replica
     (14, 37, 8, "product", "max", 1000),  # more replicas than tiles in flight
     (18, 2, 3, "random", "max", 2),       # 16 gate parts, 64 tiles
-    (14, 200, 6, "product", "max", 4),    # L2 groups of 128 + 72 replicas (QGeo::G)
-    (16, 40, 4, "random", "min", 1000),   # L2 groups of 32 + 8 replicas
+    (14, 200, 6, "product", "max", 4),    # 800 tiles per step, renormalisations inside DEC items
+    (16, 40, 4, "random", "min", 1000),
+    (20, 1, 2, "product", "max", 1000),   # one replica of config 4's chain: lag 0 over 256 tiles
 ]
 
 
@@ -216,3 +217,16 @@ def test_von_neumann_large_invariants(device, spins):
     assert np.all(vn.initial_entropy >= r2.initial_entropy - 1e-12)
     assert np.all(vn.initial_entropy <= bound) and np.all(vn.entropies <= bound) and np.all(vn.entropies >= 0)
     assert np.array_equal(vn.sites, r2.sites)  # the proposal stream does not depend on the entropy
+
+
+@pytest.mark.parametrize("spins", [16, 17])
+def test_von_neumann_large_not_normalized(device, spins):
+    """A non-unitary gate under the large-S von Neumann path (DEC items that pause the
+    producer): the reference's std::invalid_argument message, and the run without the hook is
+    clean (the paused producer is released on every DEC, failed rows included)."""
+    cfg = tg.ExperimentConfig(spins=spins, steps=3, procedures=3, seed=2, entropy_kind="von-neumann",
+                              inject_fault=2, fault_procedure=1, fault_step=1)
+    with pytest.raises(ValueError, match="entanglement_entropy: state not normalized"):
+        device.run(cfg)
+    cfg.inject_fault = 0
+    assert device.run(cfg).entropies.shape == (3, 3)
