@@ -212,9 +212,9 @@ int tg_hbm_schedule(uint32_t spins, uint64_t rows, int32_t entropy_kind);
 
 /* ---- device-piece probes (parity tests T1-T6 in SURVEY.md §4) ---------------------- */
 /* Work-queue schedule statistics (profiling probe): runs `replicas` x `steps` at `spins`
- * (13..24) on the queue schedule and writes 16 per-CTA clock64 counters per CTA into
- * stats[ctas * 16] (layout in csrc/hbm_queue.cuh, STATS); *ctas = the grid size (SM count,
- * stats must hold 16 * SM count values). */
+ * (13..24) on the queue schedule and writes 24 per-CTA clock64 counters per CTA into
+ * stats[ctas * 24] (layout in csrc/hbm_queue.cuh, STATS); *ctas = the grid size (SM count,
+ * stats must hold 24 * SM count values). */
 tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps, int32_t entropy_kind,
                                int64_t* stats, int* ctas);
 /* first n xoshiro256++ outputs of derive_stream({seed,p}) computed on the GPU */

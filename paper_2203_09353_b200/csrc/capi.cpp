@@ -917,7 +917,8 @@ tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   char* d = nullptr;
-  const size_t bytes = trace_bytes(replicas, steps, false, false) + 128 * static_cast<size_t>(sms) + 256;
+  const size_t stat_bytes = 8 * 24 * static_cast<size_t>(sms);  // hbm_queue.cuh kQStats per CTA
+  const size_t bytes = trace_bytes(replicas, steps, false, false) + stat_bytes + 256;
   TG_CUDA(cudaMalloc(&d, bytes));
   char* cur = d;
   p.initial_entropy = carve<double>(cur, replicas);
@@ -926,14 +927,14 @@ tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps
   p.status_step = carve<int64_t>(cur, replicas);
   p.entropies = carve<double>(cur, replicas * steps);
   p.accepted = carve<uint8_t>(cur, replicas * steps);
-  p.trace = carve<int64_t>(cur, 16 * static_cast<size_t>(sms));
+  p.trace = carve<int64_t>(cur, 24 * static_cast<size_t>(sms));
   const size_t wsb = workspace_for(p, dev);
   void* ws = nullptr;
   cudaError_t e = cudaMalloc(&ws, wsb);
-  if (e == cudaSuccess) e = cudaMemset(p.trace, 0, 128 * static_cast<size_t>(sms));
+  if (e == cudaSuccess) e = cudaMemset(p.trace, 0, stat_bytes);
   if (e == cudaSuccess) e = launch(p, ws, wsb, nullptr, /*trace=*/true);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e == cudaSuccess) e = cudaMemcpy(stats, p.trace, 128 * static_cast<size_t>(sms), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(stats, p.trace, stat_bytes, cudaMemcpyDeviceToHost);
   cudaFree(ws);
   cudaFree(d);
   if (e != cudaSuccess) return cuda_fail(e, "probe_queue_stats");

@@ -62,13 +62,14 @@ struct alignas(8) QMeta {  // one pipeline stage entry (written by the producer,
   Item x;  // TILE: x.r is the row; CONTROL: the item itself
 };
 
+constexpr int kQStats = 24;
 struct QHeader {
   HHeader h;
   uint64_t ctl_done;  // von Neumann: a DEC item has released the stage buffers (its scratch)
   QMeta meta[kStages];
   QRow row;          // row-state snapshot for a control item
   alignas(16) GateRec rec[2];  // control items: proposal records of steps s (decision) and s + 1 (gate)
-  int64_t stat[16];  // STATS probe only (anneal_queue_kernel<true>)
+  int64_t stat[kQStats];  // STATS probe only (anneal_queue_kernel<true>)
 };
 constexpr int kQHeaderBytes = (static_cast<int>(sizeof(QHeader)) + 127) / 128 * 128;
 constexpr int kQSmemBytes = kQHeaderBytes + kStages * kStage * 8 + 1024;
@@ -319,11 +320,13 @@ __device__ void q_renormalize(const Geo& G, double* X, double* Y, int tid, int w
   csync();
 }
 
-// STATS (probe only): per-CTA clock64 breakdown into P.trace[blockIdx.x * 16 + i]:
+// STATS (probe only): per-CTA clock64 breakdown into P.trace[blockIdx.x * kQStats + i]:
 //  0 total, 1 warp-1 waits for stage data, 2 warp-1 chunk compute, 3 warp-1 tile epilogues,
 //  4 producer waits for free stages, 5 producer dependency waits (tiles), 6 control items,
 //  7 their dependency waits, 8 tiles, 9 DEC, 10 GATE, 11 INIT + NORM items, 12 DEC clocks,
-//  13 GATE clocks, 14 producer queue pulls (atomics incl. empty slots), 15 gate passes inside DEC items
+//  13 GATE clocks, 14 producer queue pulls (atomics incl. empty slots), 15 gate passes inside DEC items,
+//  DEC phases (thread 0): 16 dependency wait + row / record loads, 17 fold + publish, 18 decision,
+//  19 renormalisation + dec_done, 20 signals after the gate
 // KIND 0: Renyi-2 (||rho||_F^2 partials); KIND 1: von Neumann for 16 <= S <= 21 (vn_large.cuh):
 // TILE items store rho to the row's planes, the DEC item diagonalises it.
 template <bool STATS = false, int KIND = 0>
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     mbar_init(&Q.ctl_done, 1);
     fence_mbar_init();
     if (STATS)
-      for (int i = 0; i < 16; ++i) Q.stat[i] = 0;
+      for (int i = 0; i < kQStats; ++i) Q.stat[i] = 0;
   }
   __syncthreads();  // the last CTA-wide barrier: from here on consumers use csync()
   static_assert(KIND == 0 || sizeof(vnl::Scratch) <= kStages * kStage * 8, "vN scratch fits the stages");
@@ -521,6 +524,7 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     }
     // DEC(r, s)
     const int64_t s = x.s;
+    const int64_t d0 = clk();
     rec_fetch(r, s);  // rec[0] = step s (the decision), rec[1] = step s + 1 (the next gate)
     if (tid == 0) {
       wait_dep(&L.tiles_done[r], q.tiles_target(s));
@@ -528,6 +532,8 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     }
     rec_wait();
     csync();
+    const int64_t d1 = clk();
+    if (STATS && tid == 0) stat_add(16, d1 - d0);
     const bool next_gate = static_cast<uint64_t>(s + 1) < P.steps;
     if (Q.row.err) {
       sync_signal(&L.dec_done[r]);
@@ -570,6 +576,8 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     q_publish(H, tid);
     double rho2, trv;
     totals<1>(H, rho2, trv);
+    const int64_t d2 = clk();
+    if (STATS && tid == 0) stat_add(17, d2 - d1);
     if constexpr (KIND == 1) {  // von Neumann: eigenvalues of this step's rho (stages = scratch)
       const size_t da = size_t{1} << G.la;
       double* Rr = L.rho + r * QLayout::rho_doubles(P.spins);
@@ -627,19 +635,24 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
       Q.row = w;
     }
     csync();
+    const int64_t d3 = clk();
+    if (STATS && tid == 0) stat_add(18, d3 - d2);
     if (s >= 0 && !Q.row.err && P.renorm > 0 && (static_cast<uint64_t>(s) + 1) % P.renorm == 0)
       q_renormalize(G, PX(r, Q.row.cur), PY(r, Q.row.cur), tid, warp, lane, H);  // spinmc.cpp:246-248
     // dec_done is waited on by GATE items only: none exist when the DEC applies the whole gate
     const bool gate_items = !q.long_dec && q.P > 1;
     if (gate_items) sync_signal(&L.dec_done[r]);
+    if (STATS && tid == 0) stat_add(19, clk() - d3);
     if (next_gate) {  // part 0 (von Neumann: every part) of the next step's gate, on the state just decided
       const int parts = q.long_dec ? static_cast<int>(q.P) : 1;
       const int64_t g0 = clk();
       if (!Q.row.err)
         for (int part = 0; part < parts; ++part) gate_part(r, Q.rec[1], part, Q.row.cur);
-      if (STATS && tid == 0) stat_add(15, clk() - g0);
+      const int64_t g1 = clk();
+      if (STATS && tid == 0) stat_add(15, g1 - g0);
       csync();
       if (tid == 0) signal(&L.gate_done[r], static_cast<unsigned long long>(parts));
+      if (STATS && tid == 0) stat_add(20, clk() - g1);
     }
   };
 
@@ -782,7 +795,7 @@ __global__ void __launch_bounds__(kQThreads, 1) anneal_queue_kernel(const Anneal
     csync();
     if (tid == 0) {
       Q.stat[0] = clk() - t_begin;
-      for (int i = 0; i < 16; ++i) P.trace[blockIdx.x * 16 + i] = Q.stat[i];
+      for (int i = 0; i < kQStats; ++i) P.trace[blockIdx.x * kQStats + i] = Q.stat[i];
     }
   }
 }
