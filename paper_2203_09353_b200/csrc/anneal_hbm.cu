@@ -638,10 +638,9 @@ cudaError_t launch_anneal_hbm(const AnnealParams& p, cudaStream_t stream, int* g
   int dev = 0, cs = 1;
   uint64_t clusters = 0;
   cudaGetDevice(&dev);
-  // the phase-trace probe runs the cluster schedule; with TG_HBM_QUEUE=1 it runs the queue's
-  // per-CTA statistics instead (tg_probe_queue_stats)
-  const char* qenv = std::getenv("TG_HBM_QUEUE");
-  const bool queue_stats = trace && qenv && qenv[0] == '1';
+  // the phase-trace probe runs the cluster schedule; tg_probe_queue_stats asks for the work
+  // queue's per-CTA statistics kernel instead
+  const bool queue_stats = trace && p.queue_stats != 0;
   if (p.rows > 0 && p.queue_rows >= p.rows &&
       (queue_stats ? queue_possible(p.spins, p.rows, p.entropy_kind)
                    : queue_pick(p.spins, p.rows, p.entropy_kind, dev, trace, p.rho_half != 0)))

@@ -901,7 +901,6 @@ tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps
                                int* ctas) {
   if (spins <= static_cast<uint32_t>(tg::kSmemMaxSpins) || spins > 24) return fail(TG_EINVAL, "queue stats cover spins in [13,24]");
   if (!stats || !ctas) return fail(TG_EINVAL, "stats / ctas must not be NULL");
-  setenv("TG_HBM_QUEUE", "1", 1);
   tg_anneal_config c{};
   c.spins = spins;
   c.devices = 1;
@@ -913,6 +912,7 @@ tg_status tg_probe_queue_stats(uint32_t spins, uint64_t replicas, uint64_t steps
   c.renormalize_interval = 1000;
   c.shard_count = 1;
   tg::AnnealParams p = make_params(&c, replicas, 0, 1);
+  p.queue_stats = 1;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
