@@ -306,7 +306,7 @@ def run_ours(args, rank, world, local_rank):
     cfg = tg.ExperimentConfig(spins=spins, steps=S, procedures=procedures, seed=0, entropy_kind=args.entropy,
                               shard_index=rank, shard_count=world, rho_half=args.rho_half)
     if args.rho_half:
-        config["rho"] = "Hermitian half (opt-in rho_half: upper-triangle 64x64 tiles, executed flops below)"
+        config["rho"] = "Hermitian half (opt-in rho_half: upper-triangle blocks, executed flops in roofline)"
     ccfg = cfg.to_c()
     rows = cfg.rows()
     L = tg.lib()
@@ -336,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
 
     peak_tflops, peak_clock = tg.fp64_dmma_peak(gpu)
     kname, ktag = anneal_kernel(L, spins, rows, args.entropy)
-    if args.rho_half:  # the option runs on the work queue only
+    if args.rho_half and spins >= 13:  # the HBM tier runs the option on the work queue only
         kname, ktag = "anneal_queue_kernel", "qh"
 
     for _ in range(args.warmup):
@@ -367,9 +367,10 @@ def run_ours(args, rank, world, local_rank):
     replica_steps = procedures * S
     value = replica_steps / t_step
     flops_launch = (rows * S + rows) * step_flops(spins)  # + initial-entropy GEMM per replica
-    if args.rho_half:  # executed flops: nt (nt + 1) / 2 of the nt^2 64x64 tiles
-        nt = (1 << (spins // 2)) // 64
-        flops_launch = flops_launch // (nt * nt) * (nt * (nt + 1) // 2)
+    if args.rho_half:  # executed flops: nb (nb + 1) / 2 of nb^2 blocks (64x64 tiles, SMEM tier: 8x8 blocks)
+        da = 1 << (spins // 2)
+        nb = da // 64 if spins >= 13 else max(da, 8) // 8
+        flops_launch = flops_launch // (nb * nb) * (nb * (nb + 1) // 2)
     achieved = flops_launch / float(np.mean(times)) / 1e12
 
     # ------------------------------------------------------------ timed: end to end (C ABI)

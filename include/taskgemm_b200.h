@@ -57,8 +57,9 @@ typedef struct {
   uint64_t renormalize_interval; /* 1000 by default; 0 disables                          */
   uint32_t shard_index, shard_count;
   uint64_t fault_procedure, fault_step;  /* inject_fault == 2 only                     */
-  int32_t rho_half;              /* opt-in, Renyi-2 with spins >= 13: form only the upper   *
-                                  * triangle of rho's 64x64 tiles (rho is Hermitian;        *
+  int32_t rho_half;              /* opt-in, Renyi-2: form only the upper triangle of rho's *
+                                  * 64x64 tiles (HBM tier) or 8x8 blocks (SMEM tier; rho is  *
+                                  * Hermitian;                                              *
                                   * ||rho||_F^2 = diagonal tiles + 2 x off-diagonal ones).  *
                                   * Not the reference's arithmetic (its GEMM is the full    *
                                   * product): entropies agree within the parity *

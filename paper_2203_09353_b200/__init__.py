@@ -232,7 +232,7 @@ class ExperimentConfig:
     inject_fault: int = 0       # 1: perturb_gemm (linalg.hpp:74-79); 2: non-unitary gate (below)
     fault_procedure: int = 0    # inject_fault == 2: this procedure's gate at fault_step is scaled by 1.001
     fault_step: int = 0
-    rho_half: bool = False      # opt-in Hermitian half of rho (Renyi-2, spins >= 13): executed flops reported apart
+    rho_half: bool = False      # opt-in Hermitian half of rho (Renyi-2): executed flops reported apart
 
     def to_c(self) -> CAnnealConfig:
         for name, table in (("entropy_kind", _ENTROPY), ("objective", _OBJECTIVE),

@@ -98,9 +98,8 @@ tg_status validate(const tg_anneal_config* c) {
                                " (d_a <= 1024); use renyi-2");
   if (c->inject_fault < 0 || c->inject_fault > 2) return fail(TG_ECONFIG, "inject_fault must be 0, 1 or 2");
   if (c->rho_half != 0 && c->rho_half != 1) return fail(TG_ECONFIG, "rho_half must be 0 or 1");
-  if (c->rho_half && (c->entropy_kind != TG_RENYI2 || c->spins <= static_cast<uint32_t>(tg::kSmemMaxSpins)))
-    return fail(TG_ECONFIG, "rho_half (Hermitian half of rho) needs renyi-2 and spins >= " +
-                                std::to_string(tg::kSmemMaxSpins + 1) + " (the HBM tier's work-queue schedule)");
+  if (c->rho_half && c->entropy_kind != TG_RENYI2)
+    return fail(TG_ECONFIG, "rho_half (Hermitian half of rho) needs renyi-2 (the eigen-solvers take the full rho)");
   if (c->objective != TG_MAXIMIZE && c->objective != TG_MINIMIZE)
     return fail(TG_ECONFIG, "objective must be max or min");
   if (c->initial_state != TG_PRODUCT && c->initial_state != TG_RANDOM)
@@ -581,9 +580,11 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
   res->average_entropy = rows ? sum / static_cast<double>(rows) : 0.0;
   res->total_flops = (rows * steps + rows) * tg_step_flops(cfg->spins);
   res->executed_flops = res->total_flops;
-  if (cfg->rho_half) {  // upper-triangle tiles only: nt (nt + 1) / 2 of nt^2
-    const uint64_t nt = (uint64_t{1} << (cfg->spins / 2)) / 64;
-    res->executed_flops = res->total_flops / (nt * nt) * (nt * (nt + 1) / 2);
+  if (cfg->rho_half) {  // upper-triangle blocks only: nb (nb + 1) / 2 of nb^2
+    // (HBM tier: 64x64 tiles; SMEM tier: 8x8 blocks of the padded d_a >= 8 rows)
+    const uint64_t da = uint64_t{1} << (cfg->spins / 2);
+    const uint64_t nb = cfg->spins > static_cast<uint32_t>(tg::kSmemMaxSpins) ? da / 64 : std::max<uint64_t>(da, 8) / 8;
+    res->executed_flops = res->total_flops / (nb * nb) * (nb * (nb + 1) / 2);
   }
   res->kernel_ms = *std::max_element(ms.begin(), ms.end());
   res->total_wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(

@@ -226,7 +226,11 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const d
 // lane), one 8-group chunk interleaved after every RATIO-th k-step of the GEMM, so its
 // DMMAs and SMEM traffic share the GEMM's pipeline instead of a separate phase. It is the
 // same DMMA computation as gate_pass_dmma: bitwise the non-speculative proposal.
-template <class D, bool STORE = false, bool SPEC = false>
+// HALF (opt-in rho_half, Renyi-2): only the upper-triangle 8x8 blocks (bi <= bj) of the
+// Hermitian rho are formed, upper block u on warp u mod 8; ||rho||_F^2 = diagonal blocks +
+// 2 x off-diagonal blocks (the doubling is exact). Trace, fault hook and the speculative gate
+// stages are unchanged.
+template <class D, bool STORE = false, bool SPEC = false, bool HALF = false>
 __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
                                              const double* __restrict__ Y, int warp, int lane,
                                              bool fault, double& rho2, double& trace,
@@ -234,13 +238,16 @@ __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
                                              int RP = 0, const GateLane* SL = nullptr,
                                              double* __restrict__ gdst = nullptr) {
   using T = Tile<D::NB>;
+  static_assert(!(HALF && STORE), "rho_half is a Renyi-2 option");
   rho2 = 0.0;
   trace = 0.0;
   constexpr int GPW = D::N / 32 / kConsumerWarps;        // gate chunks per warp
   constexpr int KI = D::DB_PAD / 4;                      // GEMM k-steps
   constexpr int RATIO = GPW > 0 && KI >= GPW ? KI / GPW : 1;
   static_assert(!SPEC || (D::SWZ && GPW >= 1 && KI % GPW == 0), "speculative gate layout");
-  if (SPEC && warp >= T::WR * T::WC) {  // warps without a GEMM tile (S < 10)
+  constexpr int NU = D::NB * (D::NB + 1) / 2;  // HALF: upper-triangle blocks
+  constexpr int GEMM_WARPS = HALF ? (NU < kConsumerWarps ? NU : kConsumerWarps) : T::WR * T::WC;
+  if (SPEC && warp >= GEMM_WARPS) {  // warps without a GEMM tile (S < 10)
 #pragma unroll 1
     for (int i = 0; i < GPW; ++i) gate_chunk<D>(*SL, X, Y, gdst, warp + kConsumerWarps * i);
   }
@@ -276,7 +283,77 @@ __device__ __forceinline__ void rho_partials(const double* __restrict__ X,
       g_vi = Y[g_cb ^ SL->kload];
     }
   };
-  if (warp < T::WR * T::WC) {
+  if constexpr (HALF) {
+    if (warp < GEMM_WARPS) {
+      constexpr int MAXB = (NU + kConsumerWarps - 1) / kConsumerWarps;
+      constexpr int NV = D::SWZ ? 4 : 1;
+      const int m = lane >> 2, kq = lane & 3;
+      int bi[MAXB], bj[MAXB];
+      bool on[MAXB];
+      int roa[MAXB][NV], rob[MAXB][NV];
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) {
+        int u = warp + kConsumerWarps * b;
+        on[b] = u < NU;
+        int r = 0;
+        while (on[b] && u >= D::NB - r) {  // upper block u, row-major
+          u -= D::NB - r;
+          ++r;
+        }
+        bi[b] = on[b] ? r : 0;
+        bj[b] = on[b] ? r + u : 0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int c = D::SWZ ? 4 * v : 0;
+          roa[b][v] = D::at(bi[b] * 8 + m, kq + c) - c * D::PITCH;
+          rob[b][v] = D::at(bj[b] * 8 + m, kq + c) - c * D::PITCH;
+        }
+      }
+      double cr[MAXB][2], ci[MAXB][2];
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) cr[b][0] = cr[b][1] = ci[b][0] = ci[b][1] = 0.0;
+#pragma unroll
+      for (int kb = 0; kb < D::DB_PAD; kb += 4) {
+        if constexpr (SPEC) spec_stage(kb / 4);
+        const int v = D::SWZ ? (((kb >> 2) ^ (kb >> 4)) & 3) : 0;
+        const int ko = kb * D::PITCH;
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) {
+          if (!on[b]) continue;
+          const double xa = X[roa[b][v] + ko], ya = Y[roa[b][v] + ko];
+          const double xb = X[rob[b][v] + ko], yb = Y[rob[b][v] + ko];
+          dmma(cr[b][0], cr[b][1], xa, xb);
+          dmma(cr[b][0], cr[b][1], ya, yb);
+          dmma(ci[b][0], ci[b][1], ya, xb);
+          dmma(ci[b][0], ci[b][1], -xa, yb);
+        }
+      }
+      if constexpr (SPEC) {
+        spec_stage(KI);
+        spec_stage(KI + 1);
+        spec_stage(KI + 2);
+      }
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b)
+        if (on[b] && bi[b] == bj[b]) {
+          if (m == 2 * kq) trace += cr[b][0];
+          if (m == 2 * kq + 1) trace += cr[b][1];
+        }
+      if (fault && warp == 0 && lane == 0) cr[0][0] -= 2.0 * (X[0] * X[0] + Y[0] * Y[0]);  // block (0,0)
+      double pd[4] = {0.0, 0.0, 0.0, 0.0}, po[4] = {0.0, 0.0, 0.0, 0.0};  // diagonal / off-diagonal chains
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (!on[b]) continue;
+          double& a = bi[b] == bj[b] ? pd[(b * 2 + e) & 3] : po[(b * 2 + e) & 3];
+          a = fma(cr[b][e], cr[b][e], a);
+          a = fma(ci[b][e], ci[b][e], a);
+        }
+      const double off = (po[0] + po[1]) + (po[2] + po[3]);
+      rho2 = ((pd[0] + pd[1]) + (pd[2] + pd[3])) + (off + off);
+    }
+  } else if (warp < T::WR * T::WC) {
     const int wr = warp / T::WC, wc = warp % T::WC;
     const int m = lane >> 2, kq = lane & 3;
     double cr[T::TM][T::TN][2], ci[T::TM][T::TN][2];

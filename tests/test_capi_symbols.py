@@ -129,11 +129,11 @@ def test_environment_switches_documented():
 
 
 def test_rho_half_validation():
-    """rho_half is a Renyi-2, HBM-tier option: anything else is a ConfigError (host-side
-    validation, no GPU needed)."""
-    ok = tg.ExperimentConfig(spins=14, steps=2, procedures=1, rho_half=True)
-    ok.validate()
-    for bad in (tg.ExperimentConfig(spins=12, steps=2, procedures=1, rho_half=True),
-                tg.ExperimentConfig(spins=14, steps=2, procedures=1, rho_half=True, entropy_kind="von-neumann")):
+    """rho_half is a Renyi-2 option (both tiers); with von Neumann it is a ConfigError
+    (host-side validation, no GPU needed)."""
+    for spins in (4, 12, 14, 20):
+        tg.ExperimentConfig(spins=spins, steps=2, procedures=1, rho_half=True).validate()
+    for bad in (tg.ExperimentConfig(spins=14, steps=2, procedures=1, rho_half=True, entropy_kind="von-neumann"),
+                tg.ExperimentConfig(spins=10, steps=2, procedures=1, rho_half=True, entropy_kind="von-neumann")):
         with pytest.raises(tg.ConfigError, match="rho_half"):
             bad.validate()
