@@ -135,6 +135,14 @@ class ClockSampler:
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
+        if not getattr(self, "lines", []):  # a timed region shorter than the 100 ms sampling period
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                      "-i", str(self.gpu)], capture_output=True, text=True, timeout=10).stdout
+                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+                self.post_run = True
+            except (OSError, subprocess.TimeoutExpired):
+                pass
         sm, mx, reasons = [], 0.0, set()
         names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
         for ln in getattr(self, "lines", []):
@@ -149,8 +157,10 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if getattr(self, "post_run", False):
+            out["note"] = "timed region shorter than the 100 ms sampling period: one reading right after it"
+        return out
 
 
 def cpu_model():
