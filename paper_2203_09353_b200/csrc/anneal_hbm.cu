@@ -610,19 +610,12 @@ cudaError_t launch_queue(const AnnealParams& p, cudaStream_t stream, int dev, in
                  : (stats ? hbmq::anneal_queue_kernel<true, 0> : hbmq::anneal_queue_kernel<false, 0>);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, hbmq::kQSmemBytes);
   if (e != cudaSuccess) return e;
-  const int grid = sms > 0 ? sms : 1;  // one CTA per SM; the queue is deadlock-free at any residency
+  const int grid = std::min(sms > 0 ? sms : 1, hbmq::QLayout::kMaxCtas);  // one CTA per SM (deadlock-free at any residency)
   if (grid_out) *grid_out = grid;
   if (std::getenv("TG_VERBOSE"))
     std::fprintf(stderr, "[tg] hbm work queue: spins %u rows %llu on %d CTAs\n", p.spins,
                  static_cast<unsigned long long>(p.rows), grid);
-  // launched as clusters of one CTA: the producer's st.async metadata writes address the
-  // CTA's shared memory as shared::cluster
-  cudaLaunchAttribute attr[1];
-  cudaLaunchConfig_t cfg = hbm_config(grid, 1, stream, attr);
-  cfg.blockDim = dim3(hbmq::kQThreads);
-  cfg.dynamicSmemBytes = hbmq::kQSmemBytes;
-  e = cudaLaunchKernelEx(&cfg, kern, p, tmap);
-  if (e != cudaSuccess) return e;
+  kern<<<grid, hbmq::kQThreads, hbmq::kQSmemBytes, stream>>>(p, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess || vn) return e;
   return launch_finish_renyi(p, stream);  // Renyi-2 traces were stored as raw ||rho||_F^2

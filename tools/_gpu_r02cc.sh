@@ -1,0 +1,3 @@
+timeout 1200 python -m pytest tests/test_queue_schedule.py -x -q 2>&1 | tail -2
+timeout 2400 python -m pytest tests/test_sanitizer.py -q 2>&1 | tail -2
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c4', d['value'], round(d['roofline']['frac'],4), d['roofline']['kernel'])"
