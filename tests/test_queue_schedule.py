@@ -235,3 +235,20 @@ def test_von_neumann_large_not_normalized(device, spins):
         device.run(cfg)
     cfg.inject_fault = 0
     assert device.run(cfg).entropies.shape == (3, 3)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("spins,procs,steps", [(20, 4, 6), (16, 8, 60), (18, 3, 12)])
+def test_queue_long_trajectories_vs_oracle(device, oracle, monkeypatch, spins, procs, steps):
+    """The headline kernel (work queue) on config 4's chain and on longer L = 16 / 18 runs,
+    against the oracle (the reference's O(d^3) CPU GEMM: ~7 s per L = 20 step on one core,
+    so the replicas run on parallel host threads): sites and accept flags bit-exact,
+    entropies within 1e-10."""
+    monkeypatch.setenv("TG_HBM_QUEUE", "1")
+    cfg = tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=77, initial_state="random")
+    rep = device.run(cfg)
+    want = oracle.run(McCfg(spins=spins, steps=steps, seed=77, initial_state=1), 0, procs)
+    assert np.array_equal(rep.sites, want.sites)
+    assert np.array_equal(rep.accepted, want.accepted)
+    assert close(rep.entropies, want.entropies).all(), np.abs(rep.entropies - want.entropies).max()
+    assert close(rep.initial_entropy, want.initial).all()
