@@ -109,6 +109,9 @@ typedef struct {
   uint64_t near_tie_capacity;
   uint64_t executed_flops;       /* out: GEMM flops the device executed (= total_flops     *
                                   * unless rho_half)                                       */
+  uint32_t nccl_ranks;           /* out: GPUs of the NCCL all-gather that fed the average   *
+                                  * (the run's one collective); 0 = host copies *
+                                  * (one GPU, GPUs repeated in the context, NCCL absent)    */
 } tg_anneal_result;
 
 /* Device-resident outputs for tg_anneal_launch (rows as above). */

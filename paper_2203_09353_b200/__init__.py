@@ -88,7 +88,7 @@ class CAnnealResult(C.Structure):
         ("device_kernel_ms", C.POINTER(C.c_double)), ("device_resident", C.POINTER(C.c_uint64)),
         ("initial_wall_ns", C.POINTER(C.c_int64)), ("fallback_decisions", C.c_uint64),
         ("near_ties", C.c_uint64), ("near_tie_log", C.POINTER(CNearTie)), ("near_tie_capacity", C.c_uint64),
-        ("executed_flops", C.c_uint64),
+        ("executed_flops", C.c_uint64), ("nccl_ranks", C.c_uint32),
     ]
 
 
@@ -291,6 +291,7 @@ class RunReport:
     near_ties: int = 0           # decisions with |u - p| < 1e-9
     near_tie_log: list = field(default_factory=list)  # NearTie, (procedure, step) order
     executed_flops: int = 0      # GEMM flops executed on the device (< total_flops with rho_half)
+    nccl_ranks: int = 0          # GPUs of the NCCL all-gather of the finals (0: host copies)
 
     def trace(self, row: int) -> EntropyTrace:
         return EntropyTrace(int(self.procedures[row]), float(self.initial_entropy[row]),
@@ -400,7 +401,7 @@ class Device:
                          res.total_flops, res.kernel_ms, device_kernel_ms=list(dms[:max(cfg.devices, 1)]),
                          device_resident=list(drs[:max(cfg.devices, 1)]), initial_wall_ns=iw,
                          fallback_decisions=res.fallback_decisions, near_ties=res.near_ties, near_tie_log=ties,
-                         executed_flops=res.executed_flops)
+                         executed_flops=res.executed_flops, nccl_ranks=res.nccl_ranks)
 
     def batched_gemm(self, a_list, b_list, c_list=None, alpha=1.0, beta=0.0, device: int = 0,
                      procedures=None, records: bool = False):

@@ -7,6 +7,8 @@
 // GPU, trace copy-back and the procedure-order average (spinmc.cpp:253-269). There is no
 // CPU fallback: without a CUDA device every entry point fails with TG_ECUDA.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -59,17 +61,47 @@ struct DeviceState {
   size_t gemm_dev_bytes = 0;
   void* gemm_pin = nullptr;
   size_t gemm_pin_bytes = 0;
+  double* gather = nullptr;  // NCCL all-gather of the final entropies: [send: maxrows][recv: D x maxrows]
+  size_t gather_bytes = 0;
 };
 
 }  // namespace
 
 struct tg_ctx {
   std::vector<DeviceState> devs;
+  std::vector<ncclComm_t> comms;  // in-process NCCL communicator over devs (distinct GPUs), lazily
+  bool comms_tried = false;
   std::mutex mu;
   bool shutdown = false;
 };
 
 namespace {
+
+// NCCL, loaded at run time: the process may already hold torch's libnccl.so.2 (same soname),
+// which dlopen then returns; linking one at build time could pin a second version first.
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+};
+const NcclApi* nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!a.h) return a;
+    a.CommInitAll = reinterpret_cast<decltype(a.CommInitAll)>(dlsym(a.h, "ncclCommInitAll"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(a.h, "ncclAllGather"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.h, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.h, "ncclGroupEnd"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.h, "ncclCommDestroy"));
+    if (!a.CommInitAll || !a.AllGather || !a.GroupStart || !a.GroupEnd || !a.CommDestroy) a.h = nullptr;
+    return a;
+  }();
+  return api.h ? &api : nullptr;
+}
 
 uint64_t rows_for(const tg_anneal_config* c) {
   const uint64_t sc = c->shard_count ? c->shard_count : 1;
@@ -298,6 +330,8 @@ tg_status tg_shutdown(tg_ctx* ctx) {
 
 tg_status tg_destroy(tg_ctx* ctx) {
   if (!ctx) return TG_OK;
+  if (const NcclApi* n = nccl_api())
+    for (ncclComm_t cm : ctx->comms) n->CommDestroy(cm);
   for (auto& d : ctx->devs) {
     cudaSetDevice(d.ordinal);
     cudaStreamSynchronize(d.stream);
@@ -305,6 +339,7 @@ tg_status tg_destroy(tg_ctx* ctx) {
     if (d.workspace) cudaFree(d.workspace);
     if (d.gemm_dev) cudaFree(d.gemm_dev);
     if (d.gemm_pin) cudaFreeHost(d.gemm_pin);
+    if (d.gather) cudaFree(d.gather);
     cudaStreamSynchronize(d.copy);
     cudaEventDestroy(d.ev0);
     cudaEventDestroy(d.ev1);
@@ -381,6 +416,7 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
   std::vector<std::vector<int64_t>> iwall(D);
   std::vector<uint64_t> resident(D, 0);
   std::vector<std::vector<double>> finals(D);
+  std::vector<double*> fin_dev(D, nullptr);  // the device copy of each GPU's final entropies
   std::vector<unsigned long long> tie_stats(2 * D, 0);
   std::vector<std::vector<tg_near_tie>> ties(D);
 
@@ -537,6 +573,7 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
       }
     }
     finals[g] = std::move(fin);
+    fin_dev[g] = p.final_entropy;
   };
 
   if (D == 1) {
@@ -574,6 +611,68 @@ tg_status tg_anneal_run(tg_ctx* ctx, const tg_anneal_config* cfg, tg_anneal_resu
     for (uint64_t g = 0; g < D; ++g) res->device_kernel_ms[g] = ms[g];
   if (res->device_resident)
     for (uint64_t g = 0; g < D; ++g) res->device_resident[g] = resident[g];
+  // The final entropies of all GPUs, for the average: one NCCL all-gather over the context's
+  // GPUs (the run's only collective), launched as a group from this thread
+  // once every GPU's anneal has finished; the host copies are the fallback (GPUs repeated in
+  // the context, NCCL unavailable, TG_NCCL=0). TG_NCCL_FORCE=1 also gathers with one GPU.
+  res->nccl_ranks = 0;
+  if (steps > 0 && (D > 1 || std::getenv("TG_NCCL_FORCE")) && !(std::getenv("TG_NCCL") && std::getenv("TG_NCCL")[0] == '0')) {
+    const NcclApi* n = nccl_api();
+    if (n && !ctx->comms_tried) {
+      ctx->comms_tried = true;
+      std::vector<int> ord(ctx->devs.size());
+      for (size_t g = 0; g < ord.size(); ++g) ord[g] = ctx->devs[g].ordinal;
+      std::vector<int> sorted = ord;
+      std::sort(sorted.begin(), sorted.end());
+      if (std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end()) {  // NCCL: one rank per GPU
+        std::vector<ncclComm_t> cm(ord.size());
+        if (n->CommInitAll(cm.data(), static_cast<int>(ord.size()), ord.data()) == ncclSuccess) ctx->comms = cm;
+      }
+    }
+    if (n && ctx->comms.size() == D) {  // every rank of the communicator takes part
+      uint64_t maxrows = 0;
+      for (uint64_t g = 0; g < D; ++g) maxrows = std::max<uint64_t>(maxrows, finals[g].size());
+      bool ok = maxrows > 0;
+      for (uint64_t g = 0; g < D && ok; ++g) {  // send buffer: this GPU's finals, zero padded
+        DeviceState& d = ctx->devs[g];
+        const size_t need = 8 * maxrows * (D + 1);
+        ok = cudaSetDevice(d.ordinal) == cudaSuccess;
+        if (ok && d.gather_bytes < need) {
+          if (d.gather) cudaFree(d.gather);
+          d.gather = nullptr;
+          d.gather_bytes = 0;
+          ok = cudaMalloc(&d.gather, need) == cudaSuccess;
+          if (ok) d.gather_bytes = need;
+        }
+        ok = ok && cudaMemsetAsync(d.gather, 0, 8 * maxrows, d.stream) == cudaSuccess &&
+             cudaMemcpyAsync(d.gather, fin_dev[g], 8 * finals[g].size(), cudaMemcpyDeviceToDevice, d.stream) ==
+                 cudaSuccess;
+      }
+      if (ok) {
+        ok = n->GroupStart() == ncclSuccess;
+        for (uint64_t g = 0; g < D && ok; ++g) {
+          DeviceState& d = ctx->devs[g];
+          ok = cudaSetDevice(d.ordinal) == cudaSuccess &&
+               n->AllGather(d.gather, d.gather + maxrows, maxrows, ncclFloat64, ctx->comms[g], d.stream) == ncclSuccess;
+        }
+        ok = (n->GroupEnd() == ncclSuccess) && ok;
+      }
+      std::vector<double> all(D * maxrows);
+      for (uint64_t g = 0; g < D && ok; ++g) {
+        DeviceState& d = ctx->devs[g];
+        ok = cudaSetDevice(d.ordinal) == cudaSuccess && cudaStreamSynchronize(d.stream) == cudaSuccess;
+      }
+      ok = ok && cudaSetDevice(ctx->devs[0].ordinal) == cudaSuccess &&
+           cudaMemcpy(all.data(), ctx->devs[0].gather + maxrows, 8 * D * maxrows, cudaMemcpyDeviceToHost) == cudaSuccess;
+      if (ok) {
+        for (uint64_t g = 0; g < D; ++g)
+          for (uint64_t q = 0; q < finals[g].size(); ++q) finals[g][q] = all[g * maxrows + q];
+        res->nccl_ranks = static_cast<uint32_t>(D);
+      } else {
+        cudaGetLastError();  // host copies stay the source of the average
+      }
+    }
+  }
   double sum = 0.0;  // procedure order, spinmc.cpp:259-268 / bench.cpp:401-407
   for (uint64_t hr = 0; hr < rows; ++hr)
     sum += steps > 0 ? finals[hr % D][hr / D] : res->initial_entropy[hr];

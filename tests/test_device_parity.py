@@ -512,3 +512,21 @@ def test_hbm_split_launch_geometry(device, oracle):
         _, ent, acc, sites, _, _ = oracle.mc_procedure(McCfg(spins=13, steps=steps, seed=9), p)
         assert np.array_equal(a.accepted[p], acc) and np.array_equal(a.sites[p], sites)
         assert close(a.entropies[p], ent).all()
+
+
+def test_nccl_gather_of_finals(monkeypatch):
+    """The in-process multi-GPU path gathers the final entropies with one NCCL all-gather
+    (C++ host code, NCCL loaded at run time). Forced on one GPU here (a one-rank
+    communicator): the average is bit for bit the host-copy path's. GPUs repeated in a context
+    (NCCL: one rank per GPU) fall back to the host copies."""
+    cfg = tg.ExperimentConfig(spins=10, steps=30, procedures=9, seed=4)
+    with tg.Device([0]) as d:
+        host = d.run(cfg)
+        monkeypatch.setenv("TG_NCCL_FORCE", "1")
+        viaccl = d.run(cfg)
+    assert host.nccl_ranks == 0 and viaccl.nccl_ranks == 1
+    assert viaccl.average_entropy == host.average_entropy
+    assert np.array_equal(viaccl.final_entropy.view(np.uint64), host.final_entropy.view(np.uint64))
+    with tg.Device([0, 0]) as d2:
+        rep = d2.run(tg.ExperimentConfig(spins=10, steps=30, procedures=9, seed=4, devices=2))
+    assert rep.nccl_ranks == 0 and rep.average_entropy == host.average_entropy
