@@ -338,6 +338,18 @@ def test_t7_config1_appendix_a(device):
     assert int(rep.accepted.sum()) == 59437
     assert list(rep.sites[0, :12]) == [0, 1, 5, 6, 2, 2, 0, 5, 4, 2, 0, 2]
     assert abs(rep.average_entropy - 2.2063680065173292) <= 1e-10 * 2.21
+    # Appendix A: the product state's initial entropy is -0.0 bit for bit (rho = |0><0| exactly,
+    # -log(1) = -0.0, and (e < 0) ? 0 : e keeps it, as std::max does), on every replica
+    assert np.all(rep.initial_entropy == 0.0) and np.all(np.signbit(rep.initial_entropy))
+    assert np.array_equal(rep.initial_entropy.view(np.uint64), g["initial"].view(np.uint64))
+
+
+@pytest.mark.parametrize("spins,queue", [(8, "0"), (12, "0"), (14, "0"), (14, "1"), (20, "1")])
+def test_product_state_initial_entropy_is_negative_zero(device, monkeypatch, spins, queue):
+    """Both tiers and both HBM schedules: -0.0 exactly for the product state, like the reference."""
+    monkeypatch.setenv("TG_HBM_QUEUE", queue)
+    rep = device.run(tg.ExperimentConfig(spins=spins, steps=1, procedures=3, seed=1))
+    assert np.all(rep.initial_entropy == 0.0) and np.all(np.signbit(rep.initial_entropy)), rep.initial_entropy
 
 
 @pytest.mark.slow
