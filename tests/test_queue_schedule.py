@@ -252,3 +252,16 @@ def test_queue_long_trajectories_vs_oracle(device, oracle, monkeypatch, spins, p
     assert np.array_equal(rep.accepted, want.accepted)
     assert close(rep.entropies, want.entropies).all(), np.abs(rep.entropies - want.entropies).max()
     assert close(rep.initial_entropy, want.initial).all()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("spins,steps", [(22, 2), (24, 1)])
+def test_queue_largest_chains_vs_cluster(device, monkeypatch, spins, steps):
+    """The largest chains (2048^3 and 4096^3 complex GEMMs) default to the work queue, all
+    SMs on one replica's tiles: bitwise the 4-CTA cluster schedule's traces, and the model's
+    choice is the queue."""
+    assert tg.lib().tg_hbm_schedule(spins, 1, 1) == 1
+    cfg = tg.ExperimentConfig(spins=spins, steps=steps, procedures=1, seed=5, initial_state="random")
+    a = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="0", TG_HBM_CTAS_PER_REPLICA="4")
+    b = run_with(device, cfg, monkeypatch)
+    assert_bitwise(a, b)
