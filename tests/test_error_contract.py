@@ -113,16 +113,20 @@ def _expected_near_ties(oracle, spins, procs, steps, eps, **kw):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("spins,kind,objective", [(6, 1, "max"), (8, 1, "min"), (12, 1, "max"), (14, 1, "max"),
-                                                  (8, 0, "max"), (13, 0, "min")])
-def test_near_tie_log_matches_oracle(oracle, monkeypatch, spins, kind, objective):
+@pytest.mark.parametrize("spins,kind,objective,queue,steps", [
+    (6, 1, "max", "0", 60), (8, 1, "min", "0", 60), (12, 1, "max", "0", 60), (14, 1, "max", "0", 60),
+    (8, 0, "max", "0", 60), (13, 0, "min", "0", 60),
+    (14, 1, "min", "1", 60), (16, 1, "max", "1", 20),   # the HBM tier's work queue (DEC items audit too)
+    (16, 0, "max", "1", 8)])                            # von Neumann on the work queue (vn_large.cuh)
+def test_near_tie_log_matches_oracle(oracle, monkeypatch, spins, kind, objective, queue, steps):
     """With the near-tie threshold widened (TG_NEAR_TIE_EPS, read per launch) the log holds
     exactly the oracle's steps with |u - p| < eps (away from the borderline), each with the
     oracle's u, p (1e-10), site and accept flag; the 1e-9 default window is derived the
     same way, so this checks the window algebra as well as the logging."""
-    eps = 2e-2
+    eps = 2e-2 if steps >= 60 else 0.2  # short runs: a wider window so that some decisions fall in it
     monkeypatch.setenv("TG_NEAR_TIE_EPS", str(eps))
-    procs, steps = 6, 60
+    monkeypatch.setenv("TG_HBM_QUEUE", queue)
+    procs = 6
     ek = "renyi-2" if kind == 1 else "von-neumann"
     with tg.Device([0]) as dev:
         rep = dev.run(tg.ExperimentConfig(spins=spins, steps=steps, procedures=procs, seed=4, entropy_kind=ek,
