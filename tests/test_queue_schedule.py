@@ -265,3 +265,30 @@ def test_queue_largest_chains_vs_cluster(device, monkeypatch, spins, steps):
     a = run_with(device, cfg, monkeypatch, TG_HBM_QUEUE="0", TG_HBM_CTAS_PER_REPLICA="4")
     b = run_with(device, cfg, monkeypatch)
     assert_bitwise(a, b)
+
+
+@pytest.mark.slow
+def test_queue_only_options_split_into_batches(device):
+    """rho_half runs on the work queue only, which takes at most 8192 rows per launch: a
+    larger run is split into batches (capi.cpp launch). Every replica still matches its own
+    run in a small batch bit for bit (traces depend only on (seed, procedure))."""
+    big = tg.ExperimentConfig(spins=14, steps=2, procedures=9000, seed=3, rho_half=True)
+    rep = device.run(big)
+    for p in (0, 8191, 8192, 8999):
+        one = device.run(tg.ExperimentConfig(spins=14, steps=2, procedures=p + 1, seed=3, rho_half=True))
+        assert np.array_equal(rep.entropies[p].view(np.uint64), one.entropies[p].view(np.uint64)), p
+        assert np.array_equal(rep.accepted[p], one.accepted[p])
+
+
+def test_queue_failing_replica_positions(device, monkeypatch):
+    """A replica that fails its norm check early (procedure 5, step 1) or late (procedure 0,
+    step 4) inside one queue launch: its remaining items are skipped while the others run to
+    the end, and the reference's message is reported."""
+    monkeypatch.setenv("TG_HBM_QUEUE", "1")
+    cfg = tg.ExperimentConfig(spins=16, steps=6, procedures=7, seed=9, inject_fault=2, fault_procedure=5,
+                              fault_step=1)
+    with pytest.raises(ValueError, match="entanglement_entropy: state not normalized"):
+        device.run(cfg)
+    cfg.fault_procedure, cfg.fault_step = 0, 4
+    with pytest.raises(ValueError, match="entanglement_entropy: state not normalized"):
+        device.run(cfg)
