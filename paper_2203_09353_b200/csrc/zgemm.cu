@@ -255,7 +255,9 @@ static_assert(16 * 4 * ZT == TPanel, "B box = one panel");
 // results are bitwise equal.
 // PROD: one extra warpgroup whose first thread issues the TMA stages (the consumer warps
 // never leave the DMMA loop to issue).
-template <int WR, int WC, int NB, int STAGES, int MINB, bool PROD = false>
+// CREGS > 0 (with PROD): setmaxnreg rebalancing, consumers up to CREGS registers and the
+// producer warpgroup 40, for shapes whose launch bound would otherwise cap the consumers.
+template <int WR, int WC, int NB, int STAGES, int MINB, bool PROD = false, int CREGS = 0>
 __global__ void __launch_bounds__(32 * WR * WC + (PROD ? 128 : 0), MINB) zgemm_tma_kernel(const ZArgs P, const __grid_constant__ CUtensorMap mapA,
                                                                       const __grid_constant__ CUtensorMap mapB) {
   constexpr int TM = 16 * WR, TN = 8 * NB * WC;
@@ -327,10 +329,12 @@ __global__ void __launch_bounds__(32 * WR * WC + (PROD ? 128 : 0), MINB) zgemm_t
     for (int j = 0; j < NB; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
   if constexpr (PROD) {
     if (tid >= 32 * WR * WC) {
+      if constexpr (CREGS > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
       if (tid == 32 * WR * WC)
         for (int64_t it = 0; it < total; ++it) issue(it);
       return;
     }
+    if constexpr (CREGS > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CREGS));
   } else if (tid == 0) {
     for (int64_t it = 0; it < STAGES - 1 && it < total; ++it) issue(it);
   }
@@ -482,16 +486,16 @@ cudaError_t launch_zgemm_strided(int batch, int m, int n, int k, double ar, doub
   // TMA staging when the shapes allow it (TG_ZGEMM_TMA=0: the cp.async pipeline)
   const char* env = std::getenv("TG_ZGEMM_TMA");
   if (!(env && env[0] == '0') && m % 8 == 0 && k % 8 == 0) {
-    // kernel shape (TG_ZGEMM_WARPS=4|8|9|16 overrides; profiles/r02_zgemm_vs_cublas.txt): the
-    // 4-warp 32x32-tile kernel (3 CTAs per SM) when 64x64 tiles would pad m x n noticeably
-    // more (96^3: 31.7 vs 18.5 TF/s), else 8 warps of 16x32 plus a producer warp that issues
+    // kernel shape (TG_ZGEMM_WARPS=4|5|8|9|16 overrides; profiles/r02_zgemm_vs_cublas.txt): the
+    // 32x32-tile kernel (3 CTAs per SM; 4 consumer warps + a producer warpgroup, "5") when
+    // 64x64 tiles would pad m x n noticeably more (96^3: 31.9 vs 18.5 TF/s), else 8 warps of 16x32 plus a producer warp that issues
     // the TMA stages ("9": best or within 0.3 % of the best at every measured size)
     auto fill = [&](int t) {
       const double mp = static_cast<double>((m + t - 1) / t * t), np_ = static_cast<double>((n + t - 1) / t * t);
       return static_cast<double>(m) * n / (mp * np_);
     };
     const char* w = std::getenv("TG_ZGEMM_WARPS");
-    const int warps = w ? std::atoi(w) : (fill(32) > 1.05 * fill(64) ? 4 : 9);
+    const int warps = w ? std::atoi(w) : (fill(32) > 1.05 * fill(64) ? 5 : 9);
     auto run = [&](auto kern, int wr, int tn, int stages, int minb, int extra = 0) -> cudaError_t {
       ZArgs Q = P;
       Q.tm = (m + 16 * wr - 1) / (16 * wr);
@@ -505,11 +509,12 @@ cudaError_t launch_zgemm_strided(int batch, int m, int n, int k, double ar, doub
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tbytes);
       if (e != cudaSuccess) return e;
       const int g = static_cast<int>(std::min<int64_t>(Q.items, static_cast<int64_t>(sms) * minb));
-      kern<<<g, 32 * wr * (warps == 4 ? 2 : warps / wr) + extra, tbytes, stream>>>(Q, mapA, mapB);
+      kern<<<g, 32 * wr * (warps == 4 || warps == 5 ? 2 : warps / wr) + extra, tbytes, stream>>>(Q, mapA, mapB);
       return cudaGetLastError();
     };
     cudaError_t e = cudaErrorNotSupported;
     if (warps == 4) e = run(zgemm_tma_kernel<2, 2, 2, 2, 3>, 2, 32, 2, 3);
+    else if (warps == 5) e = run(zgemm_tma_kernel<2, 2, 2, 2, 3, true, 120>, 2, 32, 2, 3, 128);  // 4 + producer
     else if (warps == 16) e = run(zgemm_tma_kernel<4, 4, 2, 3, 1>, 4, 64, 3, 1);
     else if (warps == 9) e = run(zgemm_tma_kernel<4, 2, 4, 3, 1, true>, 4, 64, 3, 1, 128);  // + producer
     else e = run(zgemm_tma_kernel<4, 2, 4, 3, 1>, 4, 64, 3, 1);

@@ -196,7 +196,7 @@ def test_batched_gemm_unit_epilogue_bitwise(device, monkeypatch):
     monkeypatch.setenv("TG_ZGEMM_TMA", "0")
     ref = device.batched_gemm(As, Bs)
     monkeypatch.setenv("TG_ZGEMM_TMA", "1")
-    for warps in ("4", "8", "9", "16"):
+    for warps in ("4", "5", "8", "9", "16"):
         monkeypatch.setenv("TG_ZGEMM_WARPS", warps)
         got = device.batched_gemm(As, Bs)
         for i in range(6):
@@ -218,7 +218,7 @@ def test_batched_gemm_tma_vs_cp_async_bitwise(device, monkeypatch, m, n, k, batc
     ref = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
     monkeypatch.setenv("TG_ZGEMM_TMA", "1")
     got = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
-    for warps in ("4", "8", "9", "16"):  # every warp layout of the TMA kernel (9: 8 + producer)
+    for warps in ("4", "5", "8", "9", "16"):  # every warp layout of the TMA kernel (5, 9: 4, 8 + producer)
         monkeypatch.setenv("TG_ZGEMM_WARPS", warps)
         again = device.batched_gemm(As, Bs, Cs, alpha=0.5 - 0.25j, beta=1.5 + 2j)
         for i in range(batch):

@@ -32,7 +32,7 @@ with tg.Device([0]) as d:
         A = [rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k)) for _ in range(nb)]
         B = [rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n)) for _ in range(nb)]
         Cm = [rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n)) for _ in range(nb)]
-        for w in ("4", "9", "16"):  # the TMA variants (m, k multiples of 8) and the cp.async kernel
+        for w in ("4", "5", "9", "16"):  # the TMA variants (m, k multiples of 8) and the cp.async kernel
             os.environ["TG_ZGEMM_WARPS"] = w
             out = d.batched_gemm(A, B, Cm, alpha=0.5 - 1j, beta=2.0)
             err = max(np.abs(o - ((0.5 - 1j) * a @ b + 2.0 * c)).max() for o, a, b, c in zip(out, A, B, Cm))

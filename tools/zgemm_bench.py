@@ -47,7 +47,7 @@ for m, batch in sizes:
     out = torch.empty(batch, n, m, dtype=torch.complex128, device=dev)
     fl = 8.0 * m * n * k * batch
     res, outs = {}, {}
-    for w in ("4", "8", "9", "16", "default"):
+    for w in ("4", "5", "8", "9", "16", "default"):
         if w == "default":
             os.environ.pop("TG_ZGEMM_WARPS", None)
         else:
@@ -63,7 +63,7 @@ for m, batch in sizes:
     t_cublas = timeit(lambda: torch.bmm(at, bt))
     cub = fl / t_cublas / 1e12
     print(f"{m:5d}^3 x {batch:5d}: ours {res['default']:6.2f} TF ({res['default'] / peak:5.1%} of DMMA peak, "
-          f"{res['default'] / cub:6.1%} of cuBLAS) [4w {res['4']:.2f}, 8w {res['8']:.2f}, 8w+producer {res['9']:.2f}, 16w {res['16']:.2f}], "
+          f"{res['default'] / cub:6.1%} of cuBLAS) [4w {res['4']:.2f}, 4w+producer {res['5']:.2f}, 8w {res['8']:.2f}, 8w+producer {res['9']:.2f}, 16w {res['16']:.2f}], "
           f"cuBLAS {cub:6.2f} TF, variants bitwise equal: {same}, max rel err {err:.1e}")
 
 # ---- the GEMM batcher's public API with HOST buffers (tg_zgemm_batched: copies in, kernel,

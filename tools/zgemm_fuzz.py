@@ -28,10 +28,11 @@ with tg.Device([0]) as dev:
         Cs = [rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n)) for _ in range(batch)] if be else None
         outs = {}
         for tag, env in (("cp.async", {"TG_ZGEMM_TMA": "0"}), ("tma8", {"TG_ZGEMM_TMA": "1", "TG_ZGEMM_WARPS": "8"}),
-                         ("tma16", {"TG_ZGEMM_TMA": "1", "TG_ZGEMM_WARPS": "16"}), ("tma4", {"TG_ZGEMM_TMA": "1", "TG_ZGEMM_WARPS": "4"}), ("tma9", {"TG_ZGEMM_TMA": "1", "TG_ZGEMM_WARPS": "9"})):
+                         ("tma16", {"TG_ZGEMM_TMA": "1", "TG_ZGEMM_WARPS": "16"}), ("tma4", {"TG_ZGEMM_TMA": "1", "TG_ZGEMM_WARPS": "4"}), ("tma9", {"TG_ZGEMM_TMA": "1", "TG_ZGEMM_WARPS": "9"}),
+                         ("tma5", {"TG_ZGEMM_TMA": "1", "TG_ZGEMM_WARPS": "5"})):
             os.environ.update(env)
             outs[tag] = [np.ascontiguousarray(o) for o in dev.batched_gemm(As, Bs, Cs, alpha=al, beta=be)]
-        for tag in ("tma8", "tma16", "tma4", "tma9"):
+        for tag in ("tma8", "tma16", "tma4", "tma9", "tma5"):
             for i in range(batch):
                 if not np.array_equal(outs[tag][i].view(np.uint64), outs["cp.async"][i].view(np.uint64)):
                     raise SystemExit(f"case {c} ({m}x{n}x{k} x{batch}): {tag} differs from cp.async in entry {i}")
@@ -41,4 +42,4 @@ with tg.Device([0]) as dev:
             worst = max(worst, err)
             if err > 1e-12:
                 raise SystemExit(f"case {c} ({m}x{n}x{k}): error {err}")
-print(f"{n_cases} random shapes: TMA (8 and 16 warps) bitwise equal to cp.async, max scaled error vs numpy {worst:.2e}")
+print(f"{n_cases} random shapes: TMA (4, 4+producer, 8, 8+producer, 16 warps) bitwise equal to cp.async, max scaled error vs numpy {worst:.2e}")
