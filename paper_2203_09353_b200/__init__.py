@@ -126,6 +126,23 @@ _u8p = C.POINTER(C.c_uint8)
 _lib = None
 
 
+def _pin_nccl() -> None:
+    """The C++ multi-GPU gather dlopen()s libnccl.so.2 by soname (capi.cpp nccl_api). If that
+    resolved to the system NCCL before torch is imported, torch's own libtorch_cuda.so would then
+    bind to it by the same soname and fail to load (missing newer symbols). Load the NCCL that
+    torch ships with (pip nvidia-nccl) first, when it is installed, so there is one NCCL per process."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for root in (spec.submodule_search_locations or []) if spec else []:
+        path = os.path.join(root, "nccl", "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            try:
+                C.CDLL(path, mode=C.RTLD_GLOBAL)
+            except OSError:
+                pass
+            return
+
+
 def lib() -> C.CDLL:
     """Load libtaskgemm_b200.so (fails loudly if it was not built: no fallback path)."""
     global _lib
@@ -134,6 +151,7 @@ def lib() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
                           f"g.build()'` (make -C paper_2203_09353_b200/csrc)")
+    _pin_nccl()
     L = C.CDLL(LIB_PATH)
     L.tg_last_error.restype = C.c_char_p
     L.tg_version.restype = C.c_char_p

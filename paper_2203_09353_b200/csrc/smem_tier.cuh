@@ -461,17 +461,30 @@ struct Verdict {
   int flags;
   double p;
 };
+// The part of the decision that does not depend on the new rho2 (the bound and the tie
+// window), so a caller can form it before the partials barrier.
+struct DecPre {
+  double bound, tol;
+};
 template <class R>
-__device__ __forceinline__ Verdict decide_audit(double rho2_new, double rho2_cur, const R& g, int objective,
-                                                double eps = 1e-9) {
-  const double r_new = fmin(rho2_new, 1.0), r_cur = fmin(rho2_cur, 1.0);
-  const double bound = r_cur * g.emul;
-  if (fabs(r_new - bound) > static_cast<double>(g.tie_tol) * r_new)
-    return {objective == 0 ? (r_new < bound) : (r_new > bound), 0, 0.0};
+__device__ __forceinline__ DecPre decide_prep(double rho2_cur, const R& g) {
+  return {fmin(rho2_cur, 1.0) * g.emul, static_cast<double>(g.tie_tol)};
+}
+template <class R>
+__device__ __forceinline__ Verdict decide_audit(double rho2_new, double rho2_cur, const DecPre& d, const R& g,
+                                                int objective, double eps = 1e-9) {
+  const double r_new = fmin(rho2_new, 1.0);
+  if (fabs(r_new - d.bound) > d.tol * r_new)
+    return {objective == 0 ? (r_new < d.bound) : (r_new > d.bound), 0, 0.0};
   const double proposed = renyi2(rho2_new), current = renyi2(rho2_cur);
   const double delta = objective == 0 ? proposed - current : current - proposed;
   const double p = acceptance(delta, g.temp);
   return {g.u < p, 1 | (fabs(g.u - p) < eps ? 2 : 0), p};
+}
+template <class R>
+__device__ __forceinline__ Verdict decide_audit(double rho2_new, double rho2_cur, const R& g, int objective,
+                                                double eps = 1e-9) {
+  return decide_audit(rho2_new, rho2_cur, decide_prep(rho2_cur, g), g, objective, eps);
 }
 template <class R>
 __device__ __forceinline__ int decide(double rho2_new, double rho2_cur, const R& g, int objective) {
