@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
         mbar_init(&H.full[s], 1);
         mbar_init(&H.empty[s], kWarps);
       }
+      for (int s = 0; s < 3; ++s) mbar_init(&H.gfull[s], 1);
       fence_mbar_init();
     }
     __syncthreads();
@@ -119,6 +120,18 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   const int first = static_cast<int>(rank), stride = CS;
   const bool writer = rank == 0;
   const bool light_fence = P.light_fence != 0;
+  // S >= 16, one CTA per replica: the gate pass is staged through the stage buffers by the TMA
+  // engine (gate_pass_bulk), and CTAs start a quarter step apart (b mod 4) so that the
+  // clusters' gate passes do not all hit HBM at once
+  const bool bulk_gate = TMA && CS == 1 && KIND == 0 && G0.spins >= 16 && P.gate_bulk != 0;
+  uint32_t gpar = 0;
+  if (bulk_gate && (blockIdx.x & 3) != 0) {
+    // a quarter of a step: 8 da^2 db flops at ~115 flop/clk per SM, over 4
+    const long long wait = static_cast<long long>(blockIdx.x & 3) * G0.da * G0.da / 57 * G0.db;
+    const long long t0 = clock64();
+    while (clock64() - t0 < wait) {
+    }
+  }
 
   for (uint64_t r = cid; r < P.rows; r += ncl) {
     const int64_t t_row0 = (tid == 0 && writer && P.initial_wall_ns) ? globaltimer() : 0;
@@ -176,7 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
     for (uint64_t s = 0; s < P.steps && !err; ++s) {
       const GateRec& g = H.rec[s & 1];
       mark(r, s, 0);
-      gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, kThreads);
+      if (bulk_gate)
+        gate_pass_bulk(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, stages, H.gfull, gpar);
+      else
+        gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, kThreads);
       // psi' is read by the cluster's CTAs after the barrier (bar.sync / barrier.cluster
       // release-acquire order the generic-proxy writes; no GPU-scope fence needed) and, with
       // TMA, through the async proxy

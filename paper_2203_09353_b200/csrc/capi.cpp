@@ -161,6 +161,8 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
     const double v = std::atof(e);
     if (v > 0.0 && v < 0.5) p.tie_eps = v;
   }
+  p.gate_bulk = 1;
+  if (const char* e = std::getenv("TG_GATE_BULK")) p.gate_bulk = std::atoi(e);
   p.entropy_kind = c->entropy_kind;
   p.steps = c->steps;
   p.seed = c->seed;

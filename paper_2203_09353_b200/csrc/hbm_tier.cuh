@@ -154,6 +154,120 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const d
   }
 }
 
+// Gate pass for an HBM-resident state (S >= 16, one CTA per replica), staged through the
+// drained GEMM stage buffers: the TMA engine copies chunks of kGateChunk groups (their four
+// amplitude slices, or one contiguous range when the groups span whole 2^(site+2) blocks)
+// into a 3-buffer ring (1-D bulk copies, mbarrier completion), the CTA applies the gate in
+// shared memory with gate_apply (the reference rounding: bitwise gate_pass) and bulk stores
+// write the chunk back. Per-SM bytes in flight are then bounded by the ring (128 KB) instead
+// of the threads' registers. gpar: the ring's mbarrier parities (kept across passes).
+constexpr int kGateChunk = 1024;  // groups per chunk: 4096 amplitudes = 32 KB per plane
+static_assert(3 * 8 * kGateChunk * 8 <= kStages * kStage * 8, "gate ring fits the stage buffers");
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <class R>
+__device__ void gate_pass_bulk(const double* __restrict__ sx, const double* __restrict__ sy,
+                               double* __restrict__ dx, double* __restrict__ dy, int site, const R& g,
+                               int g0, int g1, int tid, double* ring, uint64_t* bars, uint32_t& gpar) {
+  constexpr int C = kGateChunk, A = 4 * C;  // groups, amplitudes per plane of one chunk
+  double ur[16], ui[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    ur[e] = g.ur[e];
+    ui[e] = g.ui[e];
+  }
+  const int lo_mask = (1 << site) - 1;
+  auto base = [&](int gi) { return ((gi >> site) << (site + 2)) | (gi & lo_mask); };
+  const bool sliced = C <= (1 << site);  // a chunk's groups share their high bits: 4 slices
+  const int nch = (g1 - g0) / C;
+  auto buf = [&](int j) { return ring + (j % 3) * 2 * A; };  // [X: A][Y: A]
+  auto issue = [&](int j) {  // thread 0
+    double* b = buf(j);
+    uint64_t* bar = &bars[j % 3];
+    mbar_expect_tx(bar, 2 * A * 8);
+    const int gs = g0 + j * C, a0 = base(gs);
+    if (sliced) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        bulk_g2s(b + t * C, sx + a0 + (t << site), C * 8, bar);
+        bulk_g2s(b + A + t * C, sy + a0 + (t << site), C * 8, bar);
+      }
+    } else {
+      bulk_g2s(b, sx + a0, A * 8, bar);
+      bulk_g2s(b + A, sy + a0, A * 8, bar);
+    }
+  };
+  auto store = [&](int j) {  // thread 0
+    const double* b = buf(j);
+    const int gs = g0 + j * C, a0 = base(gs);
+    if (sliced) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        bulk_s2g(dx + a0 + (t << site), b + t * C, C * 8);
+        bulk_s2g(dy + a0 + (t << site), b + A + t * C, C * 8);
+      }
+    } else {
+      bulk_s2g(dx + a0, b, A * 8);
+      bulk_s2g(dy + a0, b + A, A * 8);
+    }
+    bulk_commit();
+  };
+  fence_proxy_async_smem();  // the GEMM's generic reads of the stage buffers come first
+  __syncthreads();
+  if (tid == 0) {
+    if (nch > 0) issue(0);
+    if (nch > 1) issue(1);
+  }
+  for (int j = 0; j < nch; ++j) {
+    double* b = buf(j);
+    const int q = j % 3;
+    mbar_wait(&bars[q], (gpar >> q) & 1u);
+    gpar ^= 1u << q;
+    const int gs = g0 + j * C, a0 = base(gs);
+    for (int i = tid; i < C; i += kThreads) {
+      int off[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) off[t] = sliced ? t * C + i : base(gs + i) + (t << site) - a0;
+      double vr[4], vi[4], ro[4], io[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        vr[t] = b[off[t]];
+        vi[t] = b[A + off[t]];
+      }
+      gate_apply(ur, ui, vr, vi, ro, io);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        b[off[t]] = ro[t];
+        b[A + off[t]] = io[t];
+      }
+    }
+    fence_proxy_async_smem();  // generic writes of the chunk before the bulk store reads them
+    __syncthreads();
+    if (tid == 0) {
+      store(j);
+      if (j + 2 < nch) {
+        bulk_wait_read<1>();  // chunk j-1's store has read buffer (j+2) % 3
+        issue(j + 2);
+      }
+    }
+  }
+  if (tid == 0) {
+    bulk_wait_all();  // psi' complete in global memory before the GEMM reads it
+    __threadfence();
+    fence_proxy_async_global();
+  }
+}
+
 // Issue the cp.async copies of one pipeline stage: panels of tile (ti, tj), chunk kc.
 // 4 (panel, plane) x 32 columns x 32 row-pairs = 4096 16-byte copies, 16 per thread;
 // thread tid copies row-pair rp = tid & 31 of columns 8*(i & 3) + (tid >> 5), plane-panel
@@ -529,6 +643,7 @@ struct HHeader {
   double norm_q[4];                  // renormalisation: sums over the four quarters of psi
   uint64_t full[kStages];            // TMA pipeline (rho_partials_tma)
   uint64_t empty[kStages];
+  uint64_t gfull[3];                 // staged gate pass (gate_pass_bulk): one per chunk buffer
   int32_t decision;
   int32_t error;
 };
