@@ -121,17 +121,10 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   const bool writer = rank == 0;
   const bool light_fence = P.light_fence != 0;
   // S >= 16, one CTA per replica: the gate pass is staged through the stage buffers by the TMA
-  // engine (gate_pass_bulk), and CTAs start a quarter step apart (b mod 4) so that the
-  // clusters' gate passes do not all hit HBM at once
-  const bool bulk_gate = TMA && CS == 1 && KIND == 0 && G0.spins >= 16 && P.gate_bulk != 0;
+  // engine (gate_pass_bulk). (Starting the CTAs a quarter step apart, so that their gate passes
+  // do not hit HBM together, was measured on top of it and changed nothing.)
+  const bool bulk_gate = TMA && CS == 1 && KIND == 0 && G0.spins >= P.gate_bulk_min && P.gate_bulk != 0;
   uint32_t gpar = 0;
-  if (bulk_gate && (blockIdx.x & 3) != 0) {
-    // a quarter of a step: 8 da^2 db flops at ~115 flop/clk per SM, over 4
-    const long long wait = static_cast<long long>(blockIdx.x & 3) * G0.da * G0.da / 57 * G0.db;
-    const long long t0 = clock64();
-    while (clock64() - t0 < wait) {
-    }
-  }
 
   for (uint64_t r = cid; r < P.rows; r += ncl) {
     const int64_t t_row0 = (tid == 0 && writer && P.initial_wall_ns) ? globaltimer() : 0;

@@ -163,6 +163,8 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
   }
   p.gate_bulk = 1;
   if (const char* e = std::getenv("TG_GATE_BULK")) p.gate_bulk = std::atoi(e);
+  p.gate_bulk_min = 16;
+  if (const char* e = std::getenv("TG_GATE_BULK_MIN")) p.gate_bulk_min = std::atoi(e);
   p.entropy_kind = c->entropy_kind;
   p.steps = c->steps;
   p.seed = c->seed;

@@ -234,6 +234,7 @@ __device__ void gate_pass_bulk(const double* __restrict__ sx, const double* __re
     mbar_wait(&bars[q], (gpar >> q) & 1u);
     gpar ^= 1u << q;
     const int gs = g0 + j * C, a0 = base(gs);
+#pragma unroll 2
     for (int i = tid; i < C; i += kThreads) {
       int off[4];
 #pragma unroll

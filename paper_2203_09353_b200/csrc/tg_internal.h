@@ -49,7 +49,8 @@ struct AnnealParams {
   uint64_t fault_row1;         // 1 + its row in this launch (0 = not in it; zero-init safe), per batch
   int32_t rho_half;            // Renyi-2, HBM tier, work-queue schedule only: upper-triangle tiles
   int32_t queue_stats;         // profiling probe (tg_probe_queue_stats): the work queue's STATS kernel
-  int32_t gate_bulk;           // HBM cluster schedule, S >= 16: TMA-staged gate pass (TG_GATE_BULK=0 disables)
+  int32_t gate_bulk;           // HBM cluster schedule, S >= gate_bulk_min: TMA-staged gate pass (TG_GATE_BULK=0 disables)
+  int32_t gate_bulk_min;       // (TG_GATE_BULK_MIN, default 16)
 };
 
 // Pre-generated proposal stream of one launch (gate_stream.cu).
