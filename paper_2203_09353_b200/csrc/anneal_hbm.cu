@@ -120,10 +120,11 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   const int first = static_cast<int>(rank), stride = CS;
   const bool writer = rank == 0;
   const bool light_fence = P.light_fence != 0;
-  // S >= 16, one CTA per replica: the gate pass is staged through the stage buffers by the TMA
+  // S >= 16: each CTA's share of the gate pass is staged through its stage buffers by the TMA
   // engine (gate_pass_bulk). (Starting the CTAs a quarter step apart, so that their gate passes
   // do not hit HBM together, was measured on top of it and changed nothing.)
-  const bool bulk_gate = TMA && CS == 1 && KIND == 0 && G0.spins >= P.gate_bulk_min && P.gate_bulk != 0;
+  const bool bulk_gate = TMA && KIND == 0 && G0.spins >= P.gate_bulk_min && P.gate_bulk != 0 &&
+                         (G0.n / 4 / CS) % kGateChunk == 0;
   uint32_t gpar = 0;
 
   for (uint64_t r = cid; r < P.rows; r += ncl) {
