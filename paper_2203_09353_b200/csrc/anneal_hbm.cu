@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
         mbar_init(&H.full[s], 1);
         mbar_init(&H.empty[s], kWarps);
       }
-      for (int s = 0; s < 3; ++s) mbar_init(&H.gfull[s], 1);
+      for (int s = 0; s < 8; ++s) mbar_init(&H.gfull[s], 1);
       fence_mbar_init();
     }
     __syncthreads();
@@ -123,8 +123,9 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
   // S >= 16: each CTA's share of the gate pass is staged through its stage buffers by the TMA
   // engine (gate_pass_bulk). (Starting the CTAs a quarter step apart, so that their gate passes
   // do not hit HBM together, was measured on top of it and changed nothing.)
+  const int gate_chunk = P.gate_chunk > 0 ? P.gate_chunk : kGateChunk;
   const bool bulk_gate = TMA && KIND == 0 && G0.spins >= P.gate_bulk_min && P.gate_bulk != 0 &&
-                         (G0.n / 4 / CS) % kGateChunk == 0;
+                         (G0.n / 4 / CS) % gate_chunk == 0;
   uint32_t gpar = 0;
 
   for (uint64_t r = cid; r < P.rows; r += ncl) {
@@ -184,7 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1) anneal_hbm_kernel(const AnnealPar
       const GateRec& g = H.rec[s & 1];
       mark(r, s, 0);
       if (bulk_gate)
-        gate_pass_bulk(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, stages, H.gfull, gpar);
+        gate_pass_bulk(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, stages, H.gfull, gpar,
+                       gate_chunk);
       else
         gate_pass(PX(cur), PY(cur), PX(cur ^ 1), PY(cur ^ 1), g.site, g, g0, g1, tid, kThreads);
       // psi' is read by the cluster's CTAs after the barrier (bar.sync / barrier.cluster

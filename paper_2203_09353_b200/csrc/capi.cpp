@@ -165,6 +165,11 @@ tg::AnnealParams make_params(const tg_anneal_config* c, uint64_t rows, uint64_t 
   if (const char* e = std::getenv("TG_GATE_BULK")) p.gate_bulk = std::atoi(e);
   p.gate_bulk_min = 16;
   if (const char* e = std::getenv("TG_GATE_BULK_MIN")) p.gate_bulk_min = std::atoi(e);
+  p.gate_chunk = 0;
+  if (const char* e = std::getenv("TG_GATE_CHUNK")) {
+    const int v = std::atoi(e);
+    if (v >= 64 && v <= 1024 && (v & (v - 1)) == 0) p.gate_chunk = v;
+  }
   p.entropy_kind = c->entropy_kind;
   p.steps = c->steps;
   p.seed = c->seed;

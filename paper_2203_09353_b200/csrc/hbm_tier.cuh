@@ -161,8 +161,9 @@ __device__ __forceinline__ void gate_pass(const double* __restrict__ sx, const d
 // shared memory with gate_apply (the reference rounding: bitwise gate_pass) and bulk stores
 // write the chunk back. Per-SM bytes in flight are then bounded by the ring (128 KB) instead
 // of the threads' registers. gpar: the ring's mbarrier parities (kept across passes).
-constexpr int kGateChunk = 1024;  // groups per chunk: 4096 amplitudes = 32 KB per plane
-static_assert(3 * 8 * kGateChunk * 8 <= kStages * kStage * 8, "gate ring fits the stage buffers");
+constexpr int kGateChunk = 1024;  // default groups per chunk: 4096 amplitudes = 32 KB per plane
+constexpr int kGateRingBytes = 3 * 8 * kGateChunk * 8;  // 192 KB: the ring's share of the stage buffers
+static_assert(kGateRingBytes <= kStages * kStage * 8, "gate ring fits the stage buffers");
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
                "r"(bytes)
@@ -175,11 +176,15 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// C: groups per chunk (a power of two dividing g1 - g0); the ring holds NB = min(8, 192 KB /
+// chunk bytes) chunks, NB - 1 of them in flight.
 template <class R>
 __device__ void gate_pass_bulk(const double* __restrict__ sx, const double* __restrict__ sy,
                                double* __restrict__ dx, double* __restrict__ dy, int site, const R& g,
-                               int g0, int g1, int tid, double* ring, uint64_t* bars, uint32_t& gpar) {
-  constexpr int C = kGateChunk, A = 4 * C;  // groups, amplitudes per plane of one chunk
+                               int g0, int g1, int tid, double* ring, uint64_t* bars, uint32_t& gpar,
+                               int C = kGateChunk) {
+  const int A = 4 * C;  // amplitudes per plane of one chunk
+  const int NB = min(8, kGateRingBytes / (64 * C));
   double ur[16], ui[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
@@ -190,10 +195,10 @@ __device__ void gate_pass_bulk(const double* __restrict__ sx, const double* __re
   auto base = [&](int gi) { return ((gi >> site) << (site + 2)) | (gi & lo_mask); };
   const bool sliced = C <= (1 << site);  // a chunk's groups share their high bits: 4 slices
   const int nch = (g1 - g0) / C;
-  auto buf = [&](int j) { return ring + (j % 3) * 2 * A; };  // [X: A][Y: A]
+  auto buf = [&](int j) { return ring + (j % NB) * 2 * A; };  // [X: A][Y: A]
   auto issue = [&](int j) {  // thread 0
     double* b = buf(j);
-    uint64_t* bar = &bars[j % 3];
+    uint64_t* bar = &bars[j % NB];
     mbar_expect_tx(bar, 2 * A * 8);
     const int gs = g0 + j * C, a0 = base(gs);
     if (sliced) {
@@ -224,13 +229,11 @@ __device__ void gate_pass_bulk(const double* __restrict__ sx, const double* __re
   };
   fence_proxy_async_smem();  // the GEMM's generic reads of the stage buffers come first
   __syncthreads();
-  if (tid == 0) {
-    if (nch > 0) issue(0);
-    if (nch > 1) issue(1);
-  }
+  if (tid == 0)
+    for (int j = 0; j < NB - 1 && j < nch; ++j) issue(j);
   for (int j = 0; j < nch; ++j) {
     double* b = buf(j);
-    const int q = j % 3;
+    const int q = j % NB;
     mbar_wait(&bars[q], (gpar >> q) & 1u);
     gpar ^= 1u << q;
     const int gs = g0 + j * C, a0 = base(gs);
@@ -256,9 +259,9 @@ __device__ void gate_pass_bulk(const double* __restrict__ sx, const double* __re
     __syncthreads();
     if (tid == 0) {
       store(j);
-      if (j + 2 < nch) {
-        bulk_wait_read<1>();  // chunk j-1's store has read buffer (j+2) % 3
-        issue(j + 2);
+      if (j + NB - 1 < nch) {
+        bulk_wait_read<1>();  // chunk j-1's store has read buffer (j+NB-1) % NB
+        issue(j + NB - 1);
       }
     }
   }
@@ -644,7 +647,7 @@ struct HHeader {
   double norm_q[4];                  // renormalisation: sums over the four quarters of psi
   uint64_t full[kStages];            // TMA pipeline (rho_partials_tma)
   uint64_t empty[kStages];
-  uint64_t gfull[3];                 // staged gate pass (gate_pass_bulk): one per chunk buffer
+  uint64_t gfull[8];                 // staged gate pass (gate_pass_bulk): one per chunk buffer
   int32_t decision;
   int32_t error;
 };

@@ -51,6 +51,7 @@ struct AnnealParams {
   int32_t queue_stats;         // profiling probe (tg_probe_queue_stats): the work queue's STATS kernel
   int32_t gate_bulk;           // HBM cluster schedule, S >= gate_bulk_min: TMA-staged gate pass (TG_GATE_BULK=0 disables)
   int32_t gate_bulk_min;       // (TG_GATE_BULK_MIN, default 16)
+  int32_t gate_chunk;          // groups per staged chunk (TG_GATE_CHUNK; 0 = kGateChunk)
 };
 
 // Pre-generated proposal stream of one launch (gate_stream.cu).
